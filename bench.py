@@ -1,0 +1,482 @@
+"""Benchmark: fused iterations/s of Diffuse fused windows on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bs|stencil|cg|pcg] [--no-extra]
+
+A *step* is one iteration of the workload's task stream as the unchanged
+reference front end fuses it (recorded plan, ``paper_2406_18109_b200/
+workloads``): Black-Scholes chain = 1 fused kernel (67 tasks) per iteration.
+The headline (``--workload bs``) is BASELINE configs[1] -- 1e9 fp64 options --
+per GPU (it fits one B200: 24 GB), weak-scaled over N GPUs.  ``value`` is
+device-timed with inputs resident in HBM; ``e2e`` repeats the step through the
+executor's public calls with host buffers (pinned H2D of x, y and D2H of out
+inside the timed region).  Extra keys carry the unfused run, the other
+BASELINE workloads and the CPU baseline (the oracle port of the reference's
+numpy executor on a bounded 1M-option sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WL_DIR = os.path.join(REPO, "paper_2406_18109_b200", "workloads")
+
+WORKLOADS = {
+    "bs": ("Black-Scholes chain (67-task window), 1e9 fp64 options per GPU", "bs_{mode}_c1", 1e9, 1e6),
+    "stencil": ("5-point stencil + residual, 32768^2 fp64 band per GPU", "stencil_{mode}_cpu", 32768**2, 2048**2),
+    "cg": ("CG, 2-D Poisson CSR, 8192^2 rows per GPU", "cg_{mode}_cpu", 8192**2, 1024**2),
+    "pcg": ("Jacobi-PCG (dense MULT fused with sparse reductions), 8192^2 rows per GPU", "pcg_{mode}_cpu", 8192**2, 1024**2),
+}
+
+
+def env_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def load_trace(name):
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    return PlanTrace.load(os.path.join(WL_DIR, name + ".json.gz"))
+
+
+def iteration_split(trace):
+    its = trace.iterations()
+    sig = [tuple(e.f for k, e in it if k == "exec") for it in its]
+    steady = next(i for i in range(len(its)) if sig[i] == sig[-1])
+    return its, steady
+
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active"
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
+                 "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 4:
+                self.samples.append((time.time(), parts))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        win = [s for t, s in self.samples if self.t0 and self.t1 and self.t0 - 0.03 <= t <= self.t1 + 0.03]
+        scope = "timed region"
+        if not win:
+            win = [s for _, s in self.samples[-10:]]
+            scope = "nearest samples (timed region shorter than the 20 ms sampling period)"
+        sm = [float(s[0]) for s in win if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in win if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clocks_setting"}
+        for s in win:
+            try:
+                v = int(s[3], 16)
+            except ValueError:
+                continue
+            for bit, n in names.items():
+                if v & bit:
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(win), "scope": scope}
+
+
+def run_cpu_baseline(wl, mode, budget_s=10.0):
+    """The oracle port of the reference executor on the bounded CPU sample (rank 0, N=1)."""
+    from oracle.interp import replay as oreplay
+
+    desc, cpu_name, full_units, cpu_units = WORKLOADS[wl]
+    tr = load_trace(cpu_name.format(mode=mode))
+    its, steady = iteration_split(tr)
+    heap = None
+    for it in its[:steady]:
+        heap = oreplay(tr, it, heap)
+    n = 0
+    t0 = time.perf_counter()
+    i = steady
+    while True:
+        heap = oreplay(tr, its[i], heap)
+        n += 1
+        i = i + 1 if i + 1 < len(its) else steady
+        if time.perf_counter() - t0 >= budget_s or n >= 200:
+            break
+    dt = time.perf_counter() - t0
+    its_s = n / dt
+    return {
+        "value": its_s * cpu_units / full_units,
+        "unit": "iter/s",
+        "cores": 1,
+        "kind": "port",
+        "sample": f"{n} steady iterations of {cpu_name.format(mode=mode)} ({int(cpu_units):,} units) in {dt:.1f}s "
+                  f"= {its_s:.3f} it/s, scaled linearly to {int(full_units):,} units (numpy ufuncs are single-threaded)",
+    }
+
+
+def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True):
+    """Warm-up W iterations past the ramp, then time exactly K iterations on the executor's stream."""
+    from paper_2406_18109_b200.executor import replay
+    from paper_2406_18109_b200.traffic import launch_bytes
+
+    its, steady = iteration_split(trace)
+    seq = list(range(steady)) + [steady + (i % (len(its) - steady)) for i in range(warmup + steps)]
+    for i in seq[: steady + warmup]:
+        replay(ex, its[i])
+    ex.sync()
+    timed = seq[steady + warmup:]
+    ev = []
+    n0 = ex.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(ext_stream)
+    for i in timed:
+        for k, e in its[i]:
+            if k == "exec":
+                if with_events:
+                    a = torch.cuda.Event(enable_timing=True)
+                    a.record(ext_stream)
+                ex.execute(e.task, e.kernel, e.temp_positions)
+                if with_events:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record(ext_stream)
+                    ev.append((e, a, b))
+            elif k == "free":
+                ex.free(e)
+    end.record(ext_stream)
+    ex.sync()
+    ms = start.elapsed_time(end)
+    launches = ex.launch_count() - n0
+    # dominant exec: largest summed device time
+    per = {}
+    for e, a, b in ev:
+        key = (e.task.kind, e.f)
+        d = per.setdefault(key, [e, 0.0, 0])
+        d[1] += a.elapsed_time(b)
+        d[2] += 1
+    dom = None
+    if per:
+        e, tot, cnt = max(per.values(), key=lambda d: d[1])
+        mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
+        byts = launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
+        dom = {"kind": e.task.kind, "f": e.f, "avg_ms": tot / cnt, "launches": cnt, "bytes": byts,
+               "share": tot / ms if ms else None}
+    # algorithmic bytes of one timed iteration on this rank
+    it_bytes = 0
+    for k, e in its[timed[0]]:
+        if k == "exec":
+            mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
+            it_bytes += launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
+    return ms, launches, dom, it_bytes
+
+
+def reduce_max(torch, world, x):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(torch, world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def make_executor(trace, rank, world, local, torch):
+    from paper_2406_18109_b200.executor import Executor
+
+    ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, rank=rank, world=world,
+                  device=local)
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [ex.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ex.init_comm(obj[0])
+    return ex
+
+
+def e2e_bs(ex, trace, steps, torch, ext_stream, world):
+    """Same iteration through the executor with host buffers: H2D(x, y) + fused step + D2H(out)."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2406_18109_b200.executor import replay
+    from paper_2406_18109_b200.ir import rect_of
+    from paper_2406_18109_b200.runtime import check
+
+    its, steady = iteration_split(trace)
+    step = its[steady]
+    execs = [e for k, e in step if k == "exec"]
+    t = execs[0].task
+    xs, ys = t.args[0].store, t.args[1].store
+    out = [a.store for e in execs for a in e.task.args if a.priv == "W" and a.store in trace.live][-1]
+    shape = trace.shapes[xs]
+    pts = list(t.points())
+    rects = {i: rect_of(shape, t.args[0].part, pts[i]) for i in range(len(pts))}
+    mine = [rects[i] for i in rects if ex.point_rank(i, len(pts)) == ex.rank]
+    lo, hi = min(r[0][0] for r in mine), max(r[1][0] for r in mine)
+    rect = ((lo,), (hi,))
+    n = hi - lo
+    ptrs = []
+    for _ in range(3):
+        p = ctypes.c_void_p()
+        check(ex.lib.dk_host_alloc(8 * int(np.prod(shape)), ctypes.byref(p)))
+        ptrs.append(p)
+    hx, hy, ho = (np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=shape) for p in ptrs)
+    rng = np.random.default_rng(1)
+    hx[lo:hi] = rng.integers(1, 10, size=n)
+    hy[lo:hi] = rng.integers(1, 10, size=n)
+    barrier(torch, world)
+    ex.sync()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(ext_stream)
+    for _ in range(steps):
+        ex.upload_async(xs, hx, rect)
+        ex.upload_async(ys, hy, rect)
+        replay(ex, step)
+        ex.download_local(out, ho, rect)
+    end.record(ext_stream)
+    ex.sync()
+    ms = start.elapsed_time(end)
+    for p in ptrs:
+        check(ex.lib.dk_host_free(p))
+    return ms, 16 * n, 8 * n
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2406_18109_b200 import runtime
+
+    runtime.load()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if peaks else "fallback"
+
+    def one(wl, mode, with_clock=False, with_e2e=False):
+        trace = load_trace(f"{wl}_{mode}_n{world}")
+        ex = make_executor(trace, rank, world, local, torch)
+        ext = torch.cuda.ExternalStream(ex.stream())
+        sampler = ClockSampler(local) if with_clock else None
+        try:
+            if sampler:
+                sampler.start()
+            barrier(torch, world)
+            barrier(torch, world)
+            if sampler:
+                sampler.mark("t0")
+            ms, launches, dom, it_bytes = measure(ex, trace, args.steps, args.warmup, torch, ext, rank)
+            if sampler:
+                sampler.mark("t1")
+            ms = reduce_max(torch, world, ms)
+            res = {"ms": ms, "launches": launches, "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats)}
+            if with_e2e:
+                e_ms, bi, bo = e2e_bs(ex, trace, args.steps, torch, ext, world)
+                res["e2e"] = (reduce_max(torch, world, e_ms), bi, bo)
+            return res
+        finally:
+            if sampler:
+                sampler.stop()
+                res_clock = sampler.summary()
+            ex.close()
+            if sampler:
+                one.clock = res_clock
+
+    one.clock = None
+    wl = args.workload
+    main = one(wl, "fused", with_clock=True, with_e2e=(wl == "bs"))
+    clocks = one.clock
+    K = args.steps
+    # every rank runs the same iteration over its own partition: whole-job iter/s = K / max-rank time
+    value = K / (main["ms"] / 1e3)
+    dom = main["dom"]
+    roof = None
+    if dom:
+        ach = dom["bytes"] / (dom["avg_ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "traffic": None,
+                "kernel": f"{dom['kind']} (fused window of {dom['f']} tasks)", "bytes_per_launch": dom["bytes"],
+                "avg_launch_ms": round(dom["avg_ms"], 4), "share_of_step": round(dom["share"], 3) if dom["share"] else None,
+                "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)", "traffic_source": "profiles/"}
+    out = {
+        "metric": f"fused iters/sec ({WORKLOADS[wl][0]})",
+        "value": round(value, 4),
+        "unit": "iter/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": round(main["ms"] / K, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference Heap init: default_rng([seed, sid]).integers(1,10))",
+        "config": {"workload": WORKLOADS[wl][0], "plan": f"{wl}_fused_n{world} (reference front end, recorded)",
+                   "mode": "fused", "parallelism": f"{world} launch points -> {world} GPUs (one per GPU)",
+                   "l2": "inputs larger than L2 (24 GB per step)" if wl == "bs" else "inputs larger than L2"},
+        "roofline": roof,
+        "hbm_gbs_step": round(main["it_bytes"] / (main["ms"] / K / 1e3) / 1e9, 1),
+        "gpu_launches": main["launches"],
+        "clocks": clocks,
+    }
+    if "e2e" in main:
+        e_ms, bi, bo = main["e2e"]
+        out["e2e"] = {"value": round(K / (e_ms / 1e3), 4), "unit": "iter/s", "h2d_bytes_per_step": bi,
+                      "d2h_bytes_per_step": bo,
+                      "path": "Executor.upload_async(x,y pinned) + replay(fused step) + Executor.download(out)"}
+    if not args.no_extra:
+        try:
+            un = one(wl, "unfused")
+            out["unfused"] = {"value": round(K / (un["ms"] / 1e3), 4), "ms_per_step": round(un["ms"] / K, 3),
+                              "gpu_launches": un["launches"]}
+            out["fused_over_unfused"] = round(un["ms"] / main["ms"], 3)
+        except Exception as exc:  # noqa: BLE001
+            out["unfused"] = {"error": f"{type(exc).__name__}: {exc}"}
+        others = {}
+        for w2 in [w for w in WORKLOADS if w != wl]:
+            try:
+                f = one(w2, "fused")
+                u = one(w2, "unfused")
+                d = f["dom"]
+                others[w2] = {
+                    "workload": WORKLOADS[w2][0],
+                    "fused_iter_s": round(K / (f["ms"] / 1e3), 3),
+                    "unfused_iter_s": round(K / (u["ms"] / 1e3), 3),
+                    "fused_over_unfused": round(u["ms"] / f["ms"], 3),
+                    "fused_hbm_gbs_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9, 1),
+                    "fused_hbm_frac_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9 / hbm_peak, 4),
+                    "dominant": {"kind": d["kind"], "f": d["f"], "avg_ms": round(d["avg_ms"], 4),
+                                 "gbs": round(d["bytes"] / (d["avg_ms"] / 1e3) / 1e9, 1)} if d else None,
+                }
+            except Exception as exc:  # noqa: BLE001
+                others[w2] = {"error": f"{type(exc).__name__}: {exc}"}
+        out["workloads"] = others
+    if rank == 0 and world == 1:
+        try:
+            out["cpu_baseline"] = run_cpu_baseline(wl, "fused")
+        except Exception as exc:  # noqa: BLE001
+            out["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, _ = env_dist()
+    if rank != 0:
+        return
+    wl = args.workload
+    desc, cpu_name, full_units, cpu_units = WORKLOADS[wl]
+    K, W = args.steps, args.warmup
+    from oracle.interp import replay as oreplay
+
+    tr = load_trace(cpu_name.format(mode="fused"))
+    its, steady = iteration_split(tr)
+    heap = None
+    for it in its[: steady + W]:
+        heap = oreplay(tr, it, heap)
+    t0 = time.perf_counter()
+    i = steady + W
+    for _ in range(K):
+        heap = oreplay(tr, its[i], heap)
+        i = i + 1 if i + 1 < len(its) else steady
+    dt = time.perf_counter() - t0
+    v = K / dt * cpu_units / full_units
+    print(json.dumps({
+        "impl": "reference",
+        "metric": f"fused iters/sec ({desc})",
+        "value": v,
+        "unit": "iter/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "dtype": "f64",
+        "config": {"workload": desc, "mode": "fused"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "port",
+                         "sample": f"{K} steady iterations of {cpu_name.format(mode='fused')} ({int(cpu_units):,} "
+                                   f"units, {dt / K * 1e3:.1f} ms/iter) scaled to {int(full_units):,} units"},
+        "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bs", choices=list(WORKLOADS))
+    ap.add_argument("--no-extra", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

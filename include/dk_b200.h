@@ -1,0 +1,126 @@
+/*
+ * dk_b200.h -- C ABI of the B200 execution backend for Diffuse fused tasks.
+ *
+ * The reference has no FFI: its execution path is Python
+ * (diffusekit pipeline.py:312-345 Session._execute -> executor.py:163-195
+ * execute_task -> kernels.py:717-784 interpret, over the Heap of
+ * executor.py:40-79).  This library replaces the *body* of that path; the
+ * Python side (paper_2406_18109_b200/runtime.py, ctypes) keeps the
+ * reference's call signature and exception types.  Every entry point returns
+ * DK_OK (0) or an error code; dk_last_error() describes the last failure of
+ * the calling thread.  One process drives one GPU (dk_init); the caller is a
+ * single Python thread.
+ *
+ * Mapping to the reference (file:line of what each group replaces):
+ *   dk_store_*      Heap.get / free / digest           executor.py:54-71
+ *   dk_kernel_*     interpret (vectorised + per-point)  kernels.py:717-784
+ *   dk_launch       execute_task point loop body        executor.py:192-195
+ *   dk_builtin      default_builtins MATVEC/SPMV/NORM/OPAQUE  executor.py:93-113
+ *                   + SPMV_CSR (new opaque kind)
+ *   dk_accum        Rd combine in point order            executor.py:193-195, 287-293
+ *   dk_comm_*       (new) halo / replicated-read transfers and partial-sum
+ *                   allgather between GPUs (SURVEY §5, §8 e)
+ */
+#ifndef DK_B200_H
+#define DK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DK_OK = 0,
+  DK_ERR_CUDA = 1,        /* CUDA runtime / driver failure                      */
+  DK_ERR_NVRTC = 2,       /* JIT compilation failed                             */
+  DK_ERR_ARG = 3,         /* malformed argument / program                       */
+  DK_ERR_OOM = 4,         /* device memory exhausted                            */
+  DK_ERR_STATE = 5,       /* not initialised / unknown store or handle          */
+  DK_ERR_NCCL = 6,        /* collective failure                                 */
+  DK_ERR_PRIVILEGE = 7,   /* store/reduce into a read-only parameter            */
+  DK_ERR_BOUNDS = 8,      /* offset access outside a bound sub-store            */
+  DK_ERR_UNSUPPORTED = 9  /* shape/broadcast pattern the backend rejects        */
+};
+
+enum { DK_F64 = 0, DK_I32 = 1 };
+
+/* A bound sub-store view: element pointer of the view origin plus per-dim
+ * extents and element strides (row-major store, innermost stride 1). */
+typedef struct {
+  uint64_t ptr;
+  int32_t rank;
+  int32_t dtype;
+  int64_t ext[4];
+  int64_t stride[4];
+} dk_view;
+
+const char* dk_last_error(void);
+int dk_version(void);
+
+/* process <-> GPU binding, stream, sync */
+int dk_init(int device);
+int dk_shutdown(void);
+int dk_set_stream(uint64_t stream);        /* 0 = library-owned stream */
+int dk_get_stream(uint64_t* stream);
+int dk_sync(void);
+int dk_device_info(int* sm_count, int64_t* free_bytes, int64_t* total_bytes);
+int dk_launch_count(int64_t* count);       /* kernels this library has launched */
+
+/* stores: row-major, VA reserved for the whole store, HBM backed on demand */
+int dk_store_create(int64_t sid, int rank, const int64_t* extents, int dtype);
+int dk_store_ensure(int64_t sid, int64_t elem_lo, int64_t elem_hi);
+int dk_store_free(int64_t sid);
+int dk_store_ptr(int64_t sid, uint64_t* dptr);
+int dk_store_bytes_mapped(int64_t sid, int64_t* bytes);
+/* copy the rect [lo, hi) between a full-store-shaped host array and the store */
+int dk_store_upload_rect(int64_t sid, const int64_t* lo, const int64_t* hi, const void* host);
+int dk_store_download_rect(int64_t sid, const int64_t* lo, const int64_t* hi, void* host);
+int dk_store_fill(int64_t sid, int64_t elem_lo, int64_t elem_hi, double value);
+
+/* scratch (task-local buffers, staging): stream-ordered */
+int dk_scratch_alloc(int64_t bytes, uint64_t* dptr);
+int dk_scratch_free(uint64_t dptr);
+int dk_memset_zero(uint64_t dptr, int64_t bytes);
+int dk_memcpy_d2h(void* host, uint64_t dptr, int64_t bytes);   /* synchronising */
+int dk_memcpy_h2d(uint64_t dptr, const void* host, int64_t bytes);
+int dk_host_alloc(int64_t bytes, void** host);                  /* pinned */
+int dk_host_free(void* host);
+
+/* JIT: program text (paper_2406_18109_b200.ir.KProg.wire) -> handle.
+ * Compilation to sm_100a happens at first launch per binding class. */
+int dk_kernel_compile(const char* program, int64_t len, int64_t* handle);
+int dk_kernel_source(int64_t handle, char* buf, int64_t cap, int64_t* len);
+int dk_kernel_num_reductions(int64_t handle, int* n);
+/* Device-free code generation (and optional NVRTC compile) for a binding:
+ * returns the generated CUDA source.  Used by the CPU test-suite. */
+int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews, int compile,
+                      char* buf, int64_t cap, int64_t* out_len);
+
+/* Run one launch point.  views[i] binds slot i.  totals == 0: every reduce
+ * statement accumulates into its target view in statement order; otherwise
+ * the per-statement totals are written to totals[k] (multi-GPU fold). */
+int dk_launch(int64_t handle, const dk_view* views, int nviews,
+              const double* scalars, int nscalars, uint64_t totals);
+
+/* for i in 0..nvals-1: target[...] += vals[first + i*stride]  (device values, in order) */
+int dk_accum(const dk_view* target, uint64_t vals, int64_t first, int64_t stride, int nvals);
+
+/* opaque kinds: kind = "MATVEC" | "SPMV" | "NORM" | "OPAQUE" | "SPMV_CSR" */
+int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t* writes);
+
+/* multi-GPU (NCCL over NVLink/NVSwitch); one rank per process */
+int dk_comm_unique_id(uint8_t* out128);
+int dk_comm_init(int rank, int world, const uint8_t* id128);
+int dk_comm_destroy(void);
+/* grouped point-to-point moves of store rects; dir: 0 send, 1 recv */
+int dk_comm_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs,
+                     const int64_t* los, const int64_t* his);
+/* allgather `count` doubles per rank from device ptr src into dst (world*count) */
+int dk_comm_allgather_f64(uint64_t src, uint64_t dst, int64_t count);
+int dk_comm_barrier(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,116 @@
+// Internal state shared by the runtime translation units (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dk_b200.h"
+
+namespace dk {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...);
+void set_last_error(const std::string& msg);
+
+#define DK_CUDA(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      ::dk::fail(e_ == cudaErrorMemoryAllocation ? DK_ERR_OOM : DK_ERR_CUDA, "%s: %s (%s:%d)", \
+                 #x, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define DK_CU(x)                                                                   \
+  do {                                                                             \
+    CUresult r_ = (x);                                                             \
+    if (r_ != CUDA_SUCCESS) {                                                      \
+      const char* s_ = nullptr;                                                    \
+      cuGetErrorString(r_, &s_);                                                   \
+      ::dk::fail(r_ == CUDA_ERROR_OUT_OF_MEMORY ? DK_ERR_OOM : DK_ERR_CUDA,        \
+                 "%s: %s (%s:%d)", #x, s_ ? s_ : "?", __FILE__, __LINE__);         \
+    }                                                                              \
+  } while (0)
+
+// C-ABI wrapper: run the body, convert exceptions into status codes.
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return DK_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return DK_ERR_STATE;
+  }
+}
+
+struct Mapping {
+  size_t off, size;
+  CUmemGenericAllocationHandle h;
+};
+
+struct Store {
+  int64_t sid = -1;
+  int rank = 0;
+  int64_t ext[4] = {1, 1, 1, 1};
+  int dtype = DK_F64;
+  size_t esize = 8;
+  int64_t nelem = 1;
+  size_t bytes = 0;
+  bool small = false;
+  CUdeviceptr base = 0;  // small: cudaMallocAsync; large: reserved VA
+  size_t va_size = 0;
+  std::vector<Mapping> maps;  // sorted by off, disjoint (large stores)
+};
+
+struct State {
+  bool inited = false;
+  int device = -1;
+  CUdevice cudev = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  size_t gran = 2u << 20;
+  std::unordered_map<int64_t, Store> stores;
+  std::multimap<size_t, Store> va_pool;  // freed large stores kept mapped, by va_size
+  size_t pool_bytes = 0;
+  int64_t launches = 0;
+  // collectives
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+State& st();
+void require_init();
+Store& store_of(int64_t sid);
+void store_ensure_bytes(Store& s, size_t lo, size_t hi);
+
+// kernels shared across units (dk_kernels.cu)
+void launch_accum(const dk_view& target, const double* vals, int64_t stride, int nvals, cudaStream_t s);
+void launch_builtin(const std::string& kind, const dk_view* v, int n, const int32_t* writes, cudaStream_t s);
+void launch_fill(double* p, int64_t n, double value, cudaStream_t s);
+void launch_pack(const dk_view& src, double* dst, cudaStream_t s, bool unpack);
+
+inline int64_t view_volume(const dk_view& v) {
+  int64_t n = 1;
+  for (int d = 0; d < v.rank; ++d) n *= v.ext[d];
+  return n;
+}
+
+}  // namespace dk

@@ -1,0 +1,1024 @@
+// Kernel JIT: fused-task IR -> sm_100a CUDA C++ (hand-written templates) -> NVRTC.
+//
+// Input is the slot-form program of paper_2406_18109_b200/ir.py (KProg.wire),
+// i.e. the reference's optimized Kernel (diffusekit kernels.py:134-151) with
+// names resolved.  One generated __global__ per loop nest.  Semantics follow
+// interpret() (kernels.py:717-784):
+//   * every SetTemp lives in registers; a fused window's temporaries never
+//     touch HBM (their stores were demoted to locals and scalarised by the
+//     front end, kernels.py:519-615);
+//   * operands are numpy-broadcast to the nest domain (the domain buffer's
+//     extents, kernels.py:750) -- rank-0 loads become uniform registers;
+//   * element pairs along the innermost dimension move as 16-byte
+//     LDG.E.128/STG.E.128 when the view is 16-byte aligned, else as two 8-byte
+//     accesses (the +-1 views of the stencil);
+//   * no FMA contraction: every + - * / is __d{add,sub,mul,div}_rn and NVRTC
+//     runs with --fmad=false, so a fused (s*x)+y rounds like numpy's two ufuncs;
+//   * min/max propagate NaN and return the second operand on ties like
+//     np.minimum/np.maximum; neg flips the sign bit (np.negative);
+//     comparisons give 1.0/0.0 and select tests != 0 (kernels.py:645-679);
+//   * ReduceStmt: per-thread register accumulator -> warp shuffle tree ->
+//     fixed-order block tree -> per-CTA partial -> the last CTA (ticket)
+//     folds the partials in a fixed order and performs buf[()] += total in
+//     statement order (kernels.py:765).  A scalar-valued expression adds
+//     value * volume, like np.sum on a 0-d value does not.
+// Loads hoisted ahead of the pair's stores are legal because the host rejects
+// bindings where a written view overlaps another view of the same store
+// (the fusion constraints already exclude that for fused windows,
+// fusion.py:72-122).
+
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <set>
+#include <sstream>
+
+#include "dk_internal.h"
+
+namespace dk {
+
+// ---------------------------------------------------------------- IR -----
+
+struct Expr {
+  char tag = 0;  // L P C V B N Q
+  int i = 0;
+  std::string op;
+  uint64_t bits = 0;
+  std::vector<int64_t> offs;
+  std::vector<Expr> k;
+};
+
+struct Stmt {
+  char tag = 0;  // T S A
+  int target = 0;
+  std::vector<int64_t> offs;
+  Expr e;
+};
+
+struct NestIR {
+  int dom = 0;
+  int decl_rank = 0;
+  std::vector<Stmt> stmts;
+};
+
+struct Prog {
+  int nslots = 0, nscal = 0, ntemps = 0;
+  std::vector<char> local;
+  std::vector<std::string> priv;
+  std::vector<NestIR> nests;
+  int nreduce = 0;
+};
+
+class Parser {
+ public:
+  explicit Parser(const std::string& s) {
+    std::string cur;
+    for (char c : s) {
+      if (c == '(' || c == ')') {
+        if (!cur.empty()) toks_.push_back(cur), cur.clear();
+        toks_.push_back(std::string(1, c));
+      } else if (isspace((unsigned char)c)) {
+        if (!cur.empty()) toks_.push_back(cur), cur.clear();
+      } else {
+        cur += c;
+      }
+    }
+    if (!cur.empty()) toks_.push_back(cur);
+  }
+  std::string next() {
+    if (pos_ >= toks_.size()) fail(DK_ERR_ARG, "kernel program: unexpected end");
+    return toks_[pos_++];
+  }
+  void expect(const char* t) {
+    std::string x = next();
+    if (x != t) fail(DK_ERR_ARG, "kernel program: expected '%s', got '%s'", t, x.c_str());
+  }
+  int64_t integer() {
+    std::string x = next();
+    char* end = nullptr;
+    long long v = strtoll(x.c_str(), &end, 10);
+    if (!end || *end) fail(DK_ERR_ARG, "kernel program: bad integer '%s'", x.c_str());
+    return v;
+  }
+  std::vector<int64_t> offsets() {
+    std::string x = next();
+    std::vector<int64_t> o;
+    if (x == "-") return o;
+    std::stringstream ss(x);
+    std::string part;
+    while (std::getline(ss, part, ',')) o.push_back(strtoll(part.c_str(), nullptr, 10));
+    return o;
+  }
+  Expr expr() {
+    expect("(");
+    Expr e;
+    std::string t = next();
+    if (t.size() != 1) fail(DK_ERR_ARG, "kernel program: bad expression tag '%s'", t.c_str());
+    e.tag = t[0];
+    switch (e.tag) {
+      case 'L':
+        e.i = (int)integer();
+        e.offs = offsets();
+        break;
+      case 'P':
+      case 'V':
+        e.i = (int)integer();
+        break;
+      case 'C':
+        e.bits = strtoull(next().c_str(), nullptr, 16);
+        break;
+      case 'B':
+        e.op = next();
+        e.k.push_back(expr());
+        e.k.push_back(expr());
+        break;
+      case 'N':
+        e.k.push_back(expr());
+        break;
+      case 'Q':
+        e.k.push_back(expr());
+        e.k.push_back(expr());
+        e.k.push_back(expr());
+        break;
+      default:
+        fail(DK_ERR_ARG, "kernel program: unknown expression tag '%c'", e.tag);
+    }
+    expect(")");
+    return e;
+  }
+
+ private:
+  std::vector<std::string> toks_;
+  size_t pos_ = 0;
+};
+
+static Prog parse_prog(const std::string& text) {
+  Parser p(text);
+  p.expect("DK1");
+  Prog g;
+  g.nslots = (int)p.integer();
+  g.nscal = (int)p.integer();
+  g.ntemps = (int)p.integer();
+  int nn = (int)p.integer();
+  for (int i = 0; i < g.nslots; ++i) {
+    p.expect("slot");
+    if (p.integer() != i) fail(DK_ERR_ARG, "kernel program: slots out of order");
+    p.integer();  // declared rank (actual ranks come from the bound views)
+    std::string kind = p.next();
+    g.local.push_back(kind == "L");
+    g.priv.push_back(p.next());
+  }
+  for (int n = 0; n < nn; ++n) {
+    p.expect("nest");
+    NestIR ne;
+    ne.dom = (int)p.integer();
+    ne.decl_rank = (int)p.integer();
+    int ns = (int)p.integer();
+    for (int s = 0; s < ns; ++s) {
+      Stmt st;
+      std::string t = p.next();
+      st.tag = t[0];
+      if (st.tag == 'T') {
+        st.target = (int)p.integer();
+        st.e = p.expr();
+      } else if (st.tag == 'S') {
+        st.target = (int)p.integer();
+        st.offs = p.offsets();
+        st.e = p.expr();
+      } else if (st.tag == 'A') {
+        st.target = (int)p.integer();
+        st.e = p.expr();
+        g.nreduce++;
+      } else {
+        fail(DK_ERR_ARG, "kernel program: unknown statement '%s'", t.c_str());
+      }
+      ne.stmts.push_back(std::move(st));
+    }
+    g.nests.push_back(std::move(ne));
+  }
+  p.expect("end");
+  for (auto& ne : g.nests)
+    if (ne.dom < 0 || ne.dom >= g.nslots) fail(DK_ERR_ARG, "kernel program: bad domain slot");
+  return g;
+}
+
+// ------------------------------------------------------- binding spec -----
+
+// Parameter blocks.  Must match the device-side declarations in kPrelude.
+struct DkHdr {
+  int64_t ext[4];
+  int64_t nrows, ninner, nelem;
+  uint64_t red_part, red_ticket, red_totals;
+  int64_t red_mode;
+};
+struct DkSite {
+  uint64_t p;
+  int64_t st[3];
+  int64_t sti;
+  int64_t mode;  // 0 pair-aligned contiguous, 1 contiguous, 2 broadcast, 3 strided
+};
+static_assert(sizeof(DkHdr) == 8 * 11, "DkHdr layout");
+static_assert(sizeof(DkSite) == 48, "DkSite layout");
+static_assert(sizeof(dk_view) == 80, "dk_view layout");
+
+struct Site {
+  int slot;
+  std::vector<int64_t> offs;  // empty = zero offsets
+  char cls;                   // S scalar, C contiguous inner, B broadcast inner, G strided inner
+};
+
+struct NestPlan {
+  int rank = 0;  // actual domain rank
+  std::vector<Site> sites;
+  std::vector<char> site_loaded;   // site read before any store to its slot (phase-1 load)
+  std::vector<int> red_slots;      // target slot per reduce statement (statement order)
+  std::vector<char> red_is_array;  // per reduce statement
+  int n_array_red = 0;
+};
+
+static bool nonzero(const std::vector<int64_t>& o) {
+  for (auto v : o)
+    if (v) return true;
+  return false;
+}
+
+static void walk_loads(const Expr& e, const std::function<void(const Expr&)>& f) {
+  if (e.tag == 'L') f(e);
+  for (auto& c : e.k) walk_loads(c, f);
+}
+
+// per-dim strides of a view broadcast against the domain shape (numpy rules)
+static bool bcast_strides(const dk_view& v, const int64_t* D, int r, int64_t* out) {
+  if (v.rank > r) {
+    for (int d = 0; d < v.rank - r; ++d)
+      if (v.ext[d] != 1) return false;
+  }
+  for (int j = 0; j < r; ++j) {
+    int jj = j - (r - v.rank);
+    if (jj < 0) {
+      out[j] = 0;
+    } else if (v.ext[jj] == D[j]) {
+      out[j] = D[j] == 1 ? 0 : v.stride[jj];
+    } else if (v.ext[jj] == 1) {
+      out[j] = 0;
+    } else {
+      return false;
+    }
+  }
+  return true;
+}
+
+static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std::string* key) {
+  std::vector<NestPlan> plans;
+  std::ostringstream ks;
+  for (size_t n = 0; n < g.nests.size(); ++n) {
+    const NestIR& ne = g.nests[n];
+    const dk_view& dv = views[ne.dom];
+    NestPlan np;
+    np.rank = dv.rank;
+    const int r = dv.rank;
+    int64_t D[4] = {1, 1, 1, 1};
+    for (int d = 0; d < r; ++d) D[d] = dv.ext[d];
+    std::set<int> stored;
+    std::vector<char> temp_array(g.ntemps, 0);
+    std::function<bool(const Expr&)> is_array = [&](const Expr& e) -> bool {
+      if (e.tag == 'L') return views[e.i].rank > 0;
+      if (e.tag == 'V') return e.i < (int)temp_array.size() && temp_array[e.i];
+      for (auto& c : e.k)
+        if (is_array(c)) return true;
+      return false;
+    };
+    auto site_of = [&](int slot, const std::vector<int64_t>& offs) -> int {
+      std::vector<int64_t> o = nonzero(offs) ? offs : std::vector<int64_t>();
+      for (size_t i = 0; i < np.sites.size(); ++i)
+        if (np.sites[i].slot == slot && np.sites[i].offs == o) return (int)i;
+      Site s;
+      s.slot = slot;
+      s.offs = o;
+      const dk_view& v = views[slot];
+      if (v.dtype != DK_F64) fail(DK_ERR_UNSUPPORTED, "kernel access to a non-f64 store (slot %d)", slot);
+      if (v.rank == 0) {
+        s.cls = 'S';
+      } else {
+        int64_t str[4];
+        if (!bcast_strides(v, D, r, str))
+          fail(DK_ERR_UNSUPPORTED, "operands could not be broadcast together (slot %d rank %d vs domain rank %d)",
+               slot, v.rank, r);
+        int64_t inner = r ? str[r - 1] : 0;
+        s.cls = inner == 1 ? 'C' : inner == 0 ? 'B' : 'G';
+      }
+      if (!o.empty()) {
+        if ((int)o.size() != r || v.rank != r)
+          fail(DK_ERR_UNSUPPORTED, "offset access with mismatched ranks (slot %d)", slot);
+        for (int d = 0; d < r; ++d)
+          if (D[d] > 0 && (o[d] < 0 || o[d] + D[d] > v.ext[d]))
+            fail(DK_ERR_BOUNDS, "access at offset %lld outside buffer slot %d extent %lld", (long long)o[d], slot,
+                 (long long)v.ext[d]);
+      }
+      np.sites.push_back(s);
+      return (int)np.sites.size() - 1;
+    };
+    for (const Stmt& stt : ne.stmts) {
+      walk_loads(stt.e, [&](const Expr& ld) {
+        if (ld.i < 0 || ld.i >= g.nslots) fail(DK_ERR_ARG, "load of bad slot");
+        if (stored.count(ld.i) && nonzero(ld.offs))
+          fail(DK_ERR_UNSUPPORTED, "offset load of a buffer written in the same nest");
+        for (int rs : np.red_slots)
+          if (rs == ld.i) fail(DK_ERR_UNSUPPORTED, "nest reads a buffer it reduces into");
+        if (!stored.count(ld.i)) {
+          int si = site_of(ld.i, ld.offs);
+          if ((int)np.site_loaded.size() <= si) np.site_loaded.resize(si + 1, 0);
+          np.site_loaded[si] = 1;
+        }
+      });
+      if (stt.tag == 'T') {
+        if (stt.target >= g.ntemps) fail(DK_ERR_ARG, "bad temp index");
+        temp_array[stt.target] = is_array(stt.e);
+      } else if (stt.tag == 'S') {
+        const std::string& pv = g.priv[stt.target];
+        if (!g.local[stt.target] && pv != "W" && pv != "RW")
+          fail(DK_ERR_PRIVILEGE, "store to read-only param (slot %d)", stt.target);
+        if (nonzero(stt.offs)) fail(DK_ERR_UNSUPPORTED, "store with non-zero offsets");
+        const dk_view& tv = views[stt.target];
+        if (tv.rank != r) fail(DK_ERR_UNSUPPORTED, "store target rank %d differs from nest rank %d", tv.rank, r);
+        for (int d = 0; d < r; ++d)
+          if (tv.ext[d] != D[d]) fail(DK_ERR_UNSUPPORTED, "store target extents differ from the nest domain");
+        if (r > 0 && !is_array(stt.e)) {
+          // broadcast scalar value: still a plain pair store
+        }
+        stored.insert(stt.target);
+        int si = site_of(stt.target, {});
+        if (np.sites[si].cls == 'B') fail(DK_ERR_UNSUPPORTED, "store into a broadcast view");
+      } else {
+        const std::string& pv = g.priv[stt.target];
+        if (!g.local[stt.target] && pv != "W" && pv != "RW" && pv != "Rd")
+          fail(DK_ERR_PRIVILEGE, "reduce into read-only param (slot %d)", stt.target);
+        if (views[stt.target].dtype != DK_F64) fail(DK_ERR_UNSUPPORTED, "reduce into non-f64 view");
+        bool arr = is_array(stt.e);
+        if (arr && r == 0) fail(DK_ERR_UNSUPPORTED, "array-valued reduction in a rank-0 nest");
+        np.red_slots.push_back(stt.target);
+        np.red_is_array.push_back(arr);
+        if (arr) np.n_array_red++;
+        for (int sl : stored)
+          if (sl == stt.target) fail(DK_ERR_UNSUPPORTED, "reduce into a buffer stored in the same nest");
+      }
+    }
+    np.site_loaded.resize(np.sites.size(), 0);
+    for (const Site& s : np.sites) {
+      if (r == 0 && s.cls != 'S') fail(DK_ERR_UNSUPPORTED, "rank-0 nest over an array operand");
+    }
+    ks << "n" << n << ":r" << r << ":";
+    for (const Site& s : np.sites) {
+      ks << s.slot << s.cls;
+      for (auto o : s.offs) ks << "," << o;
+      ks << ";";
+    }
+    for (size_t k = 0; k < np.red_slots.size(); ++k) ks << "R" << np.red_slots[k] << (np.red_is_array[k] ? "a" : "s");
+    ks << "|";
+    plans.push_back(std::move(np));
+  }
+  *key = ks.str();
+  return plans;
+}
+
+// ------------------------------------------------------------ codegen -----
+
+static const char* kPrelude = R"DK(
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+struct dk_view { uint64_t ptr; int32_t rank; int32_t dtype; int64_t ext[4]; int64_t stride[4]; };
+struct DkHdr { int64_t ext[4]; int64_t nrows, ninner, nelem; uint64_t red_part, red_ticket, red_totals; int64_t red_mode; };
+struct DkSite { uint64_t p; int64_t st[3]; int64_t sti; int64_t mode; };
+
+__device__ __forceinline__ double dk_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dk_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dk_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dk_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dk_pow(double a, double b) { return pow(a, b); }
+__device__ __forceinline__ bool dk_isnan(double a) { return a != a; }
+__device__ __forceinline__ double dk_min(double a, double b) { return dk_isnan(a) ? a : (a < b ? a : b); }
+__device__ __forceinline__ double dk_max(double a, double b) { return dk_isnan(a) ? a : (a > b ? a : b); }
+__device__ __forceinline__ double dk_lt(double a, double b) { return a < b ? 1.0 : 0.0; }
+__device__ __forceinline__ double dk_le(double a, double b) { return a <= b ? 1.0 : 0.0; }
+__device__ __forceinline__ double dk_eq(double a, double b) { return a == b ? 1.0 : 0.0; }
+__device__ __forceinline__ double dk_neg(double a) {
+  return __longlong_as_double(__double_as_longlong(a) ^ (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ double dk_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+__device__ __forceinline__ double2 dk_ldp(const DkSite& s, int64_t ro, int64_t e, bool full) {
+  const double* p = (const double*)s.p + ro;
+  double2 v;
+  if (s.mode == 0) {
+    if (full) return *reinterpret_cast<const double2*>(p + e);
+    v.x = p[e]; v.y = 0.0; return v;
+  }
+  if (s.mode == 1) { v.x = p[e]; v.y = full ? p[e + 1] : 0.0; return v; }
+  if (s.mode == 2) { v.x = p[0]; v.y = v.x; return v; }
+  v.x = p[e * s.sti]; v.y = full ? p[(e + 1) * s.sti] : 0.0; return v;
+}
+
+__device__ __forceinline__ void dk_stp(const DkSite& s, int64_t ro, int64_t e, bool full, double x, double y) {
+  double* p = (double*)s.p + ro;
+  if (s.mode == 0) {
+    if (full) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; }
+    else p[e] = x;
+    return;
+  }
+  if (s.mode == 1) { p[e] = x; if (full) p[e + 1] = y; return; }
+  p[e * s.sti] = x; if (full) p[(e + 1) * s.sti] = y;
+}
+
+__device__ __forceinline__ double dk_warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double dk_ldcg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__device__ void dk_view_add(const dk_view& t, double v) {
+  int64_t n = 1;
+  for (int d = 0; d < t.rank; ++d) n *= t.ext[d];
+  double* p = (double*)t.ptr;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t o = 0, rem = i;
+    for (int d = t.rank - 1; d >= 0; --d) { o += (rem % t.ext[d]) * t.stride[d]; rem /= t.ext[d]; }
+    p[o] = __dadd_rn(p[o], v);
+  }
+}
+)DK";
+
+static const int kUnroll = 2;
+static const int kTPB = 256;
+
+class Gen {
+ public:
+  Gen(const Prog& g, const std::vector<NestPlan>& plans) : g_(g), plans_(plans) {}
+
+  std::string source() {
+    std::ostringstream o;
+    o << kPrelude;
+    for (size_t n = 0; n < g_.nests.size(); ++n) nest(o, (int)n);
+    return o.str();
+  }
+
+ private:
+  const Prog& g_;
+  const std::vector<NestPlan>& plans_;
+
+  int site_index(const NestPlan& np, int slot, const std::vector<int64_t>& offs) const {
+    std::vector<int64_t> o = nonzero(offs) ? offs : std::vector<int64_t>();
+    for (size_t i = 0; i < np.sites.size(); ++i)
+      if (np.sites[i].slot == slot && np.sites[i].offs == o) return (int)i;
+    fail(DK_ERR_STATE, "internal: no site for slot %d", slot);
+  }
+
+  static const char* binfn(const std::string& op) {
+    if (op == "+") return "dk_add";
+    if (op == "-") return "dk_sub";
+    if (op == "*") return "dk_mul";
+    if (op == "/") return "dk_div";
+    if (op == "**") return "dk_pow";
+    if (op == "min") return "dk_min";
+    if (op == "max") return "dk_max";
+    if (op == "lt") return "dk_lt";
+    if (op == "le") return "dk_le";
+    if (op == "eq") return "dk_eq";
+    fail(DK_ERR_ARG, "unknown binary op '%s'", op.c_str());
+  }
+
+  // lane: "x" / "y" for element pair lanes, "s" for scalar (epilogue / rank-0)
+  std::string expr(const NestPlan& np, const Expr& e, const std::string& lane, const std::set<int>& stored) const {
+    char buf[64];
+    switch (e.tag) {
+      case 'L': {
+        if (stored.count(e.i)) return "w" + std::to_string(e.i) + "_" + lane;
+        int si = site_index(np, e.i, e.offs);
+        const Site& s = np.sites[si];
+        if (s.cls == 'S') return "S" + std::to_string(si);
+        if (s.cls == 'B' || lane == "s") return "v" + std::to_string(si) + "[u].x";
+        return "v" + std::to_string(si) + "[u]." + lane;
+      }
+      case 'P':
+        return "P.sc[" + std::to_string(e.i) + "]";
+      case 'C':
+        snprintf(buf, sizeof buf, "dk_bits(0x%016llxULL)", (unsigned long long)e.bits);
+        return buf;
+      case 'V':
+        return "t" + std::to_string(e.i) + "_" + lane;
+      case 'B':
+        return std::string(binfn(e.op)) + "(" + expr(np, e.k[0], lane, stored) + ", " + expr(np, e.k[1], lane, stored) + ")";
+      case 'N':
+        return "dk_neg(" + expr(np, e.k[0], lane, stored) + ")";
+      case 'Q':
+        return "((" + expr(np, e.k[0], lane, stored) + ") != 0.0 ? (" + expr(np, e.k[1], lane, stored) + ") : (" +
+               expr(np, e.k[2], lane, stored) + "))";
+    }
+    fail(DK_ERR_ARG, "bad expression");
+  }
+
+  void nest(std::ostringstream& o, int n) const {
+    const NestIR& ne = g_.nests[n];
+    const NestPlan& np = plans_[n];
+    const int r = np.rank;
+    const int NS = (int)np.sites.size();
+    const int NR = (int)np.red_slots.size();
+    o << "\nstruct P" << n << " { DkHdr h; DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
+      << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ") dk_n" << n << "(const P" << n << " P) {\n";
+    // hoisted rank-0 operands
+    for (int i = 0; i < NS; ++i)
+      if (np.sites[i].cls == 'S') o << "  const double S" << i << " = *(const double*)P.s[" << i << "].p;\n";
+    // stored slots list
+    std::vector<int> wslots;
+    for (const Stmt& s : ne.stmts)
+      if (s.tag == 'S' && std::find(wslots.begin(), wslots.end(), s.target) == wslots.end()) wslots.push_back(s.target);
+
+    if (r == 0) {
+      // a single evaluation, performed by one thread
+      o << "  if (blockIdx.x != 0 || threadIdx.x != 0 || threadIdx.y != 0) return;\n";
+      o << "  const int u = 0; (void)u;\n";
+      for (int w : wslots) o << "  double w" << w << "_s = 0.0;\n";
+      emit_scalar_seq(o, np, ne, /*apply_reduce=*/true, wslots);
+      o << "}\n";
+      return;
+    }
+
+    for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
+    o << "  const int64_t nrows = P.h.nrows, ninner = P.h.ninner, npairs = (ninner + 1) >> 1;\n";
+    o << "  const int TX = blockDim.x;\n";
+    o << "  for (int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; row < nrows; row += (int64_t)gridDim.y * blockDim.y) {\n";
+    // outer indices of this row
+    if (r >= 2) {
+      o << "    int64_t oi[3] = {0, 0, 0};\n";
+      o << "    { int64_t rem = row;\n";
+      for (int d = r - 2; d >= 0; --d) o << "      oi[" << d << "] = rem % P.h.ext[" << d << "]; rem /= P.h.ext[" << d << "];\n";
+      o << "    }\n";
+    }
+    for (int i = 0; i < NS; ++i) {
+      if (np.sites[i].cls == 'S') continue;
+      o << "    const int64_t ro" << i << " = 0";
+      for (int d = 0; d < r - 1; ++d) o << " + oi[" << d << "] * P.s[" << i << "].st[" << d << "]";
+      o << ";\n";
+    }
+    o << "    for (int64_t q0 = (int64_t)blockIdx.x * TX * " << kUnroll << " + threadIdx.x; q0 < npairs; q0 += (int64_t)gridDim.x * TX * " << kUnroll << ") {\n";
+    // phase 1: loads
+    for (int i = 0; i < NS; ++i) {
+      if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
+      o << "      double2 v" << i << "[" << kUnroll << "];\n";
+    }
+    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n";
+    o << "        const int64_t q = q0 + (int64_t)u * TX;\n";
+    o << "        if (q < npairs) {\n          const int64_t e = 2 * q; const bool full = e + 1 < ninner;\n";
+    for (int i = 0; i < NS; ++i) {
+      if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
+      o << "          v" << i << "[u] = dk_ldp(P.s[" << i << "], ro" << i << ", e, full);\n";
+    }
+    o << "        }\n      }\n";
+    // phase 2: compute + store
+    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n";
+    o << "        const int64_t q = q0 + (int64_t)u * TX;\n";
+    o << "        if (q < npairs) {\n        const int64_t e = 2 * q; const bool full = e + 1 < ninner;\n";
+    for (int w : wslots) o << "        double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
+    o << "        {\n" << lane_code(np, ne, "x") << "        }\n";
+    o << "        if (full) {\n" << lane_code(np, ne, "y") << "        }\n";
+    for (int w : wslots) {
+      int si = site_index(np, w, {});
+      o << "        dk_stp(P.s[" << si << "], ro" << si << ", e, full, w" << w << "_x, w" << w << "_y);\n";
+    }
+    o << "        }\n      }\n";
+    o << "    }\n  }\n";
+    if (NR) emit_reduce_epilogue(o, np, ne, wslots);
+    o << "}\n";
+  }
+
+  // one lane's statement sequence; temps are block-scoped (re-definition safe)
+  std::string lane_code(const NestPlan& np, const NestIR& ne, const std::string& lane) const {
+    std::ostringstream o;
+    std::set<int> stored;
+    int k = 0, ka = 0;
+    // SetTemp may redefine a temp name; give every definition a fresh C++ name
+    std::vector<int> ver(g_.ntemps, 0);
+    std::function<std::string(const Expr&)> ex = [&](const Expr& e) -> std::string {
+      if (e.tag == 'V') return "t" + std::to_string(e.i) + "v" + std::to_string(ver[e.i]) + "_" + lane;
+      if (e.tag == 'B')
+        return std::string(binfn(e.op)) + "(" + ex(e.k[0]) + ", " + ex(e.k[1]) + ")";
+      if (e.tag == 'N') return "dk_neg(" + ex(e.k[0]) + ")";
+      if (e.tag == 'Q') return "((" + ex(e.k[0]) + ") != 0.0 ? (" + ex(e.k[1]) + ") : (" + ex(e.k[2]) + "))";
+      return expr(np, e, lane, stored);
+    };
+    for (const Stmt& s : ne.stmts) {
+      if (s.tag == 'T') {
+        std::string rhs = ex(s.e);
+        ver[s.target]++;
+        o << "          const double t" << s.target << "v" << ver[s.target] << "_" << lane << " = " << rhs << ";\n";
+      } else if (s.tag == 'S') {
+        o << "          w" << s.target << "_" << lane << " = " << ex(s.e) << ";\n";
+        stored.insert(s.target);
+      } else {
+        if (np.red_is_array[k]) {
+          o << "          racc" << ka << " = dk_add(racc" << ka << ", " << ex(s.e) << ");\n";
+          ka++;
+        }
+        k++;
+      }
+    }
+    return o.str();
+  }
+
+  // scalar-valued statement sequence (rank-0 nest, or the epilogue's scalar reduces)
+  void emit_scalar_seq(std::ostringstream& o, const NestPlan& np, const NestIR& ne, bool rank0,
+                       const std::vector<int>& wslots) const {
+    std::set<int> stored;
+    std::vector<int> ver(g_.ntemps, 0);
+    std::vector<char> tarr(g_.ntemps, 0);
+    std::function<bool(const Expr&)> is_arr = [&](const Expr& e) -> bool {
+      if (e.tag == 'L') {
+        if (stored.count(e.i)) return false;
+        return np.sites[site_index(np, e.i, e.offs)].cls != 'S';
+      }
+      if (e.tag == 'V') return tarr[e.i];
+      for (auto& c : e.k)
+        if (is_arr(c)) return true;
+      return false;
+    };
+    std::function<std::string(const Expr&)> ex = [&](const Expr& e) -> std::string {
+      if (e.tag == 'V') return "t" + std::to_string(e.i) + "v" + std::to_string(ver[e.i]) + "_s";
+      if (e.tag == 'B') return std::string(binfn(e.op)) + "(" + ex(e.k[0]) + ", " + ex(e.k[1]) + ")";
+      if (e.tag == 'N') return "dk_neg(" + ex(e.k[0]) + ")";
+      if (e.tag == 'Q') return "((" + ex(e.k[0]) + ") != 0.0 ? (" + ex(e.k[1]) + ") : (" + ex(e.k[2]) + "))";
+      return expr(np, e, "s", stored);
+    };
+    int k = 0, ka = 0;
+    for (const Stmt& s : ne.stmts) {
+      if (s.tag == 'T') {
+        bool arr = is_arr(s.e);
+        if (!arr) {
+          std::string rhs = ex(s.e);
+          ver[s.target]++;
+          o << "    const double t" << s.target << "v" << ver[s.target] << "_s = " << rhs << ";\n";
+        }
+        tarr[s.target] = arr;
+      } else if (s.tag == 'S') {
+        if (rank0) {
+          o << "    w" << s.target << "_s = " << ex(s.e) << ";\n";
+          stored.insert(s.target);
+        }
+      } else {
+        bool arr = np.red_is_array[k];
+        o << "    {\n";
+        if (arr) {
+          o << "      const double tot = dk_tot[" << ka << "];\n";
+          ka++;
+        } else {
+          o << "      const double tot = dk_mul(" << ex(s.e) << ", (double)P.h.nelem);\n";
+        }
+        o << "      if (P.h.red_mode == 0) dk_view_add(P.rd[" << k << "], tot); else ((double*)P.h.red_totals)[" << k
+          << "] = tot;\n    }\n";
+        k++;
+      }
+    }
+    if (rank0) {
+      for (int w : wslots) {
+        int si = site_index(np, w, {});
+        o << "    *(double*)P.s[" << si << "].p = w" << w << "_s;\n";
+      }
+    }
+  }
+
+  void emit_reduce_epilogue(std::ostringstream& o, const NestPlan& np, const NestIR& ne,
+                            const std::vector<int>& wslots) const {
+    const int NA = std::max(np.n_array_red, 1);
+    o << "  __shared__ double dk_sred[" << NA << "][8];\n  __shared__ int dk_last;\n";
+    o << "  const int lin = threadIdx.y * blockDim.x + threadIdx.x, wid = lin >> 5, lane = lin & 31;\n";
+    o << "  const int64_t G = (int64_t)gridDim.x * gridDim.y, blin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;\n";
+    o << "  double* red_part = (double*)P.h.red_part;\n";
+    for (int a = 0; a < np.n_array_red; ++a)
+      o << "  { double v = dk_warp_sum(racc" << a << "); if (lane == 0) dk_sred[" << a << "][wid] = v; }\n";
+    o << "  __syncthreads();\n";
+    o << "  if (lin == 0) {\n";
+    for (int a = 0; a < np.n_array_red; ++a)
+      o << "    { double s = 0.0; for (int w = 0; w < 8; ++w) s = dk_add(s, dk_sred[" << a << "][w]); red_part[" << a
+        << " * G + blin] = s; }\n";
+    o << "    __threadfence();\n";
+    o << "    unsigned int t = atomicAdd((unsigned int*)P.h.red_ticket, 1u);\n";
+    o << "    dk_last = (t == (unsigned int)(G - 1));\n  }\n  __syncthreads();\n";
+    o << "  if (!dk_last) return;\n  __threadfence();\n";
+    o << "  double dk_tot[" << NA << "];\n";
+    for (int a = 0; a < np.n_array_red; ++a) {
+      o << "  { double s = 0.0; for (int64_t i = lin; i < G; i += 256) s = dk_add(s, dk_ldcg(red_part + " << a
+        << " * G + i)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0) dk_sred[" << a << "][wid] = s; }\n";
+    }
+    o << "  __syncthreads();\n";
+    for (int a = 0; a < np.n_array_red; ++a)
+      o << "  { double s = 0.0; for (int w = 0; w < 8; ++w) s = dk_add(s, dk_sred[" << a << "][w]); dk_tot[" << a
+        << "] = s; }\n";
+    o << "  if (lin != 0) return;\n";
+    o << "  const int u = 0; (void)u;\n";
+    emit_scalar_seq(o, np, ne, false, wslots);
+    o << "  *(unsigned int*)P.h.red_ticket = 0u;\n";
+  }
+};
+
+// -------------------------------------------------------------- NVRTC -----
+
+static uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+static std::string cache_dir() {
+  const char* d = getenv("DK_JIT_CACHE");
+  if (d && *d) return d;
+  const char* home = getenv("HOME");
+  return std::string(home ? home : "/tmp") + "/.cache/dk_b200_jit";
+}
+
+static std::string compile_cubin(const std::string& src, std::string* log_out) {
+  static const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-lineinfo", "--std=c++17",
+                               "-default-device"};
+  const int nopt = sizeof(opts) / sizeof(opts[0]);
+  std::string key = src;
+  for (int i = 0; i < nopt; ++i) key += opts[i];
+  char name[64];
+  snprintf(name, sizeof name, "%016llx.cubin", (unsigned long long)fnv1a(key + "dk-jit-v1"));
+  std::string dir = cache_dir();
+  std::string path = dir + "/" + name;
+  {
+    std::ifstream f(path, std::ios::binary);
+    if (f) {
+      std::stringstream ss;
+      ss << f.rdbuf();
+      std::string bin = ss.str();
+      if (!bin.empty()) return bin;
+    }
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "dk_fused.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    fail(DK_ERR_NVRTC, "nvrtcCreateProgram failed");
+  nvrtcResult rc = nvrtcCompileProgram(prog, nopt, opts);
+  size_t logsz = 0;
+  nvrtcGetProgramLogSize(prog, &logsz);
+  std::string log(logsz, '\0');
+  if (logsz) nvrtcGetProgramLog(prog, &log[0]);
+  if (log_out) *log_out = log;
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    fail(DK_ERR_NVRTC, "NVRTC: %s\n%s", nvrtcGetErrorString(rc), log.c_str());
+  }
+  size_t n = 0;
+  if (nvrtcGetCUBINSize(prog, &n) != NVRTC_SUCCESS) fail(DK_ERR_NVRTC, "nvrtcGetCUBINSize failed");
+  std::string bin(n, '\0');
+  nvrtcGetCUBIN(prog, &bin[0]);
+  nvrtcDestroyProgram(&prog);
+  // best-effort disk cache
+  std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+  if (system(mk.c_str()) == 0) {
+    std::string tmp = path + ".tmp" + std::to_string((long long)getpid());
+    std::ofstream f(tmp, std::ios::binary);
+    if (f) {
+      f.write(bin.data(), (std::streamsize)bin.size());
+      f.close();
+      rename(tmp.c_str(), path.c_str());
+    }
+  }
+  return bin;
+}
+
+struct Module {
+  CUmodule mod = nullptr;
+  std::vector<CUfunction> fn;
+  std::vector<int> occ;
+  std::vector<NestPlan> plans;
+  std::vector<double*> red_part;
+  std::vector<unsigned int*> ticket;
+  std::string src;
+};
+
+struct KernelObj {
+  Prog prog;
+  std::string text;
+  std::unordered_map<std::string, std::unique_ptr<Module>> mods;
+  std::string last_src;
+};
+
+static std::vector<std::unique_ptr<KernelObj>> g_kernels;
+
+static Module* get_module(KernelObj& k, const dk_view* views) {
+  std::string key;
+  std::vector<NestPlan> plans = plan_nests(k.prog, views, &key);
+  auto it = k.mods.find(key);
+  if (it != k.mods.end()) return it->second.get();
+  auto m = std::make_unique<Module>();
+  Gen gen(k.prog, plans);
+  m->src = gen.source();
+  k.last_src = m->src;
+  std::string log;
+  std::string bin = compile_cubin(m->src, &log);
+  DK_CU(cuModuleLoadData(&m->mod, bin.data()));
+  const int sms = st().sm_count;
+  for (size_t n = 0; n < k.prog.nests.size(); ++n) {
+    CUfunction f;
+    std::string nm = "dk_n" + std::to_string(n);
+    DK_CU(cuModuleGetFunction(&f, m->mod, nm.c_str()));
+    int occ = 1;
+    DK_CU(cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kTPB, 0));
+    occ = std::max(occ, 1);
+    m->fn.push_back(f);
+    m->occ.push_back(occ);
+    double* rp = nullptr;
+    unsigned int* tk = nullptr;
+    const int na = std::max(plans[n].n_array_red, 1);
+    if (!plans[n].red_slots.empty()) {
+      DK_CUDA(cudaMalloc(&rp, sizeof(double) * (size_t)na * (size_t)sms * occ + 64));
+      DK_CUDA(cudaMalloc(&tk, sizeof(unsigned int) * 4));
+      DK_CUDA(cudaMemset(tk, 0, sizeof(unsigned int) * 4));
+    }
+    m->red_part.push_back(rp);
+    m->ticket.push_back(tk);
+  }
+  m->plans = std::move(plans);
+  Module* raw = m.get();
+  k.mods.emplace(key, std::move(m));
+  return raw;
+}
+
+static int64_t pow2ceil(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+static void launch(KernelObj& k, const dk_view* views, int nviews, const double* scalars, int nscal, uint64_t totals) {
+  const Prog& g = k.prog;
+  if (nviews != g.nslots) fail(DK_ERR_ARG, "launch binds %d views, kernel has %d slots", nviews, g.nslots);
+  if (nscal != g.nscal) fail(DK_ERR_ARG, "launch passes %d scalars, kernel expects %d", nscal, g.nscal);
+  Module* m = get_module(k, views);
+  State& S = st();
+  int kbase = 0;
+  std::vector<char> blob;
+  for (size_t n = 0; n < g.nests.size(); ++n) {
+    const NestPlan& np = m->plans[n];
+    const dk_view& dv = views[g.nests[n].dom];
+    const int r = np.rank;
+    DkHdr h = {};
+    for (int d = 0; d < 4; ++d) h.ext[d] = 1;
+    int64_t D[4] = {1, 1, 1, 1};
+    h.nelem = 1;
+    for (int d = 0; d < r; ++d) {
+      h.ext[d] = D[d] = dv.ext[d];
+      h.nelem *= dv.ext[d];
+    }
+    h.ninner = r ? D[r - 1] : 1;
+    h.nrows = 1;
+    for (int d = 0; d + 1 < r; ++d) h.nrows *= D[d];
+    h.red_part = (uint64_t)m->red_part[n];
+    h.red_ticket = (uint64_t)m->ticket[n];
+    h.red_totals = totals ? totals + 8ull * kbase : 0;
+    h.red_mode = totals ? 1 : 0;
+    const int NS = (int)np.sites.size(), NR = (int)np.red_slots.size();
+    std::vector<DkSite> sites(std::max(NS, 1));
+    memset(sites.data(), 0, sizeof(DkSite) * sites.size());
+    for (int i = 0; i < NS; ++i) {
+      const Site& s = np.sites[i];
+      const dk_view& v = views[s.slot];
+      DkSite& o = sites[i];
+      int64_t str[4] = {0, 0, 0, 0};
+      if (v.rank > 0) bcast_strides(v, D, r, str);
+      int64_t shift = 0;
+      for (size_t d = 0; d < s.offs.size(); ++d) shift += s.offs[d] * v.stride[d];
+      o.p = v.ptr + 8ull * (uint64_t)shift;
+      for (int d = 0; d < 3 && d + 1 < r; ++d) o.st[d] = str[d];
+      o.sti = r ? str[r - 1] : 0;
+      if (s.cls == 'S' || s.cls == 'B') {
+        o.mode = 2;
+      } else if (s.cls == 'G') {
+        o.mode = 3;
+      } else {
+        bool al = (o.p % 16) == 0;
+        for (int d = 0; d + 1 < r; ++d)
+          if (str[d] % 2) al = false;
+        o.mode = al ? 0 : 1;
+      }
+    }
+    std::vector<dk_view> rd(std::max(NR, 1));
+    memset(rd.data(), 0, sizeof(dk_view) * rd.size());
+    for (int q = 0; q < NR; ++q) rd[q] = views[np.red_slots[q]];
+    const size_t nsc = std::max(g.nscal, 1);
+    blob.assign(sizeof(DkHdr) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc, 0);
+    char* p = blob.data();
+    memcpy(p, &h, sizeof h);
+    p += sizeof h;
+    memcpy(p, sites.data(), sizeof(DkSite) * sites.size());
+    p += sizeof(DkSite) * sites.size();
+    memcpy(p, rd.data(), sizeof(dk_view) * rd.size());
+    p += sizeof(dk_view) * rd.size();
+    if (g.nscal) memcpy(p, scalars, 8 * (size_t)g.nscal);
+    // launch shape
+    unsigned gx = 1, gy = 1, tx = kTPB, ty = 1;
+    if (r > 0 && h.nelem > 0) {
+      const int64_t npairs = (h.ninner + 1) / 2;
+      tx = (unsigned)(npairs >= kTPB ? kTPB : std::max<int64_t>(32, pow2ceil(npairs)));
+      ty = kTPB / tx;
+      const int64_t maxg = (int64_t)S.sm_count * m->occ[n];
+      int64_t GX = std::min<int64_t>((npairs + (int64_t)tx * kUnroll - 1) / ((int64_t)tx * kUnroll), maxg);
+      GX = std::max<int64_t>(GX, 1);
+      int64_t GY = std::min<int64_t>((h.nrows + ty - 1) / ty, std::max<int64_t>(1, maxg / GX));
+      GY = std::min<int64_t>(std::max<int64_t>(GY, 1), 65535);
+      gx = (unsigned)GX;
+      gy = (unsigned)GY;
+    } else if (r == 0) {
+      tx = 32;
+      ty = 1;
+    }
+    size_t bsz = blob.size();
+    void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &bsz,
+                     CU_LAUNCH_PARAM_END};
+    DK_CU(cuLaunchKernel(m->fn[n], gx, gy, 1, tx, ty, 1, 0, (CUstream)S.stream, nullptr, extra));
+    S.launches++;
+    kbase += NR;
+  }
+}
+
+}  // namespace dk
+
+using namespace dk;
+
+extern "C" {
+
+int dk_kernel_compile(const char* program, int64_t len, int64_t* handle) {
+  return guard([&] {
+    require_init();
+    auto k = std::make_unique<KernelObj>();
+    k->text.assign(program, (size_t)len);
+    k->prog = parse_prog(k->text);
+    g_kernels.push_back(std::move(k));
+    *handle = (int64_t)g_kernels.size() - 1;
+  });
+}
+
+static KernelObj& kernel_of(int64_t h) {
+  if (h < 0 || h >= (int64_t)g_kernels.size()) fail(DK_ERR_STATE, "unknown kernel handle %lld", (long long)h);
+  return *g_kernels[h];
+}
+
+int dk_kernel_source(int64_t handle, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    KernelObj& k = kernel_of(handle);
+    *len = (int64_t)k.last_src.size();
+    if (buf && cap > 0) {
+      int64_t n = std::min<int64_t>(cap - 1, *len);
+      memcpy(buf, k.last_src.data(), (size_t)n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews, int compile, char* buf,
+                      int64_t cap, int64_t* out_len) {
+  return guard([&] {
+    Prog g = parse_prog(std::string(program, (size_t)len));
+    if (nviews != g.nslots) fail(DK_ERR_ARG, "codegen binds %d views, kernel has %d slots", nviews, g.nslots);
+    std::string key;
+    std::vector<NestPlan> plans = plan_nests(g, views, &key);
+    Gen gen(g, plans);
+    std::string src = gen.source();
+    if (compile) {
+      std::string log;
+      std::string bin = compile_cubin(src, &log);
+      if (bin.empty()) fail(DK_ERR_NVRTC, "empty cubin");
+    }
+    *out_len = (int64_t)src.size();
+    if (buf && cap > 0) {
+      int64_t n = std::min<int64_t>(cap - 1, *out_len);
+      memcpy(buf, src.data(), (size_t)n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int dk_kernel_num_reductions(int64_t handle, int* n) {
+  return guard([&] { *n = kernel_of(handle).prog.nreduce; });
+}
+
+int dk_launch(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+              uint64_t totals) {
+  return guard([&] {
+    require_init();
+    launch(kernel_of(handle), views, nviews, scalars, nscalars, totals);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// Precompiled sm_100a kernels: ordered reduction combine, opaque builtins,
+// fills and rect pack/unpack for transfers.
+//
+// Builtins restate diffusekit executor.py:93-113 on the GPU:
+//   MATVEC / SPMV (dense a2 = a0 @ a1)  -- one warp per output row
+//   NORM  (a1 += sum(a0 * a0))          -- deterministic two-level tree
+//   OPAQUE (W/RW args += 1.0)
+// plus the new SPMV_CSR kind: per row, acc = 0.0 then
+// acc = acc + vals[j] * x[cols[j]] left to right -- bit-identical to the
+// oracle's definition because the order and the roundings are the same and
+// __dmul_rn/__dadd_rn forbid FMA contraction.
+
+#include <string>
+
+#include "dk_internal.h"
+
+namespace dk {
+
+struct VIdx {
+  // element offset of the i-th element (row-major order) of a view
+  __device__ static int64_t off(const dk_view& v, int64_t i) {
+    int64_t o = 0;
+    for (int d = v.rank - 1; d >= 0; --d) {
+      int64_t e = v.ext[d];
+      o += (i % e) * v.stride[d];
+      i /= e;
+    }
+    return o;
+  }
+};
+
+__global__ void k_accum(dk_view t, const double* __restrict__ vals, int64_t stride, int nvals) {
+  int64_t n = 1;
+  for (int d = 0; d < t.rank; ++d) n *= t.ext[d];
+  double* p = (double*)t.ptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double* q = p + VIdx::off(t, i);
+    double a = *q;
+    for (int k = 0; k < nvals; ++k) a = __dadd_rn(a, vals[k * stride]);
+    *q = a;
+  }
+}
+
+void launch_accum(const dk_view& target, const double* vals, int64_t stride, int nvals, cudaStream_t s) {
+  int64_t n = view_volume(target);
+  if (n == 0) return;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+  k_accum<<<blocks, 256, 0, s>>>(target, vals, stride, nvals);
+  DK_CUDA(cudaGetLastError());
+  st().launches++;
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+void launch_fill(double* p, int64_t n, double value, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)st().sm_count * 8);
+  k_fill<<<blocks, 256, 0, s>>>(p, n, value);
+  DK_CUDA(cudaGetLastError());
+  st().launches++;
+}
+
+// pack a strided view into a dense buffer (unpack: the reverse); 8-byte elements
+__global__ void k_pack(dk_view v, double* buf, int unpack) {
+  int64_t n = 1;
+  for (int d = 0; d < v.rank; ++d) n *= v.ext[d];
+  double* p = (double*)v.ptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = VIdx::off(v, i);
+    if (unpack)
+      p[o] = buf[i];
+    else
+      buf[i] = p[o];
+  }
+}
+
+void launch_pack(const dk_view& src, double* dst, cudaStream_t s, bool unpack) {
+  int64_t n = view_volume(src);
+  if (n == 0) return;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)st().sm_count * 8);
+  k_pack<<<blocks, 256, 0, s>>>(src, dst, unpack ? 1 : 0);
+  DK_CUDA(cudaGetLastError());
+  st().launches++;
+}
+
+// ---- SPMV_CSR ---------------------------------------------------------------
+
+template <class I>
+__global__ void __launch_bounds__(256) k_spmv_csr(const I* __restrict__ rowptr, const I* __restrict__ cols,
+                                                  const double* __restrict__ vals, const double* __restrict__ x,
+                                                  double* __restrict__ y, int64_t nrows) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = (int64_t)rowptr[i], e = (int64_t)rowptr[i + 1];
+    double acc = 0.0;
+    for (int64_t j = b; j < e; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + j), __ldg(x + (int64_t)cols[j])));
+    y[i] = acc;
+  }
+}
+
+// ---- dense matvec: one warp per row, fixed lane order ------------------------
+
+__global__ void k_matvec(dk_view A, dk_view xv, dk_view yv) {
+  const int64_t m = A.ext[0], k = A.ext[1];
+  const double* a = (const double*)A.ptr;
+  const double* x = (const double*)xv.ptr;
+  double* y = (double*)yv.ptr;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = warp; row < m; row += nw) {
+    double acc = 0.0;
+    for (int64_t j = lane; j < k; j += 32)
+      acc = __dadd_rn(acc, __dmul_rn(a[row * A.stride[0] + j * A.stride[1]], x[j * xv.stride[0]]));
+    for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) y[row * yv.stride[0]] = acc;
+  }
+}
+
+// ---- NORM: target += sum(x*x), single block, fixed order ---------------------
+
+__global__ void k_norm(dk_view xv, dk_view t) {
+  __shared__ double sh[32];
+  int64_t n = 1;
+  for (int d = 0; d < xv.rank; ++d) n *= xv.ext[d];
+  const double* x = (const double*)xv.ptr;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = x[VIdx::off(xv, i)];
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = __dadd_rn(s, sh[w]);
+    int64_t nt = 1;
+    for (int d = 0; d < t.rank; ++d) nt *= t.ext[d];
+    double* tp = (double*)t.ptr;
+    for (int64_t i = 0; i < nt; ++i) {
+      double* q = tp + VIdx::off(t, i);
+      *q = __dadd_rn(*q, s);
+    }
+  }
+}
+
+__global__ void k_add_one(dk_view v) {
+  int64_t n = 1;
+  for (int d = 0; d < v.rank; ++d) n *= v.ext[d];
+  double* p = (double*)v.ptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double* q = p + VIdx::off(v, i);
+    *q = __dadd_rn(*q, 1.0);
+  }
+}
+
+static void check_f64(const dk_view& v, const char* what) {
+  if (v.dtype != DK_F64) fail(DK_ERR_UNSUPPORTED, "%s: expected an f64 view", what);
+}
+
+void launch_builtin(const std::string& kind, const dk_view* v, int n, const int32_t* writes, cudaStream_t s) {
+  const int sms = st().sm_count;
+  if (kind == "SPMV_CSR") {
+    if (n != 5) fail(DK_ERR_ARG, "SPMV_CSR expects 5 args, got %d", n);
+    const dk_view &rp = v[0], &cl = v[1], &vl = v[2], &x = v[3], &y = v[4];
+    check_f64(vl, "SPMV_CSR vals");
+    check_f64(x, "SPMV_CSR x");
+    check_f64(y, "SPMV_CSR y");
+    if (rp.dtype != cl.dtype) fail(DK_ERR_UNSUPPORTED, "SPMV_CSR rowptr/cols dtypes differ");
+    for (int i = 0; i < 5; ++i)
+      if (v[i].rank > 1 && view_volume(v[i]) > 0) {
+        // only contiguous rank-1 segments are supported (row-band tiles)
+        for (int d = 0; d + 1 < v[i].rank; ++d)
+          if (v[i].ext[d] != 1) fail(DK_ERR_UNSUPPORTED, "SPMV_CSR arg %d is not a contiguous segment", i);
+      }
+    const int64_t nrows = view_volume(y);
+    if (view_volume(rp) != nrows + 1 && !(nrows == 0 && view_volume(rp) <= 1))
+      fail(DK_ERR_ARG, "SPMV_CSR: rowptr has %lld entries for %lld rows", (long long)view_volume(rp), (long long)nrows);
+    if (nrows == 0) return;
+    int blocks = (int)std::min<int64_t>((nrows + 255) / 256, (int64_t)sms * 8);
+    if (rp.dtype == DK_I32)
+      k_spmv_csr<int32_t><<<blocks, 256, 0, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
+                                                  (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr, nrows);
+    else
+      k_spmv_csr<double><<<blocks, 256, 0, s>>>((const double*)rp.ptr, (const double*)cl.ptr,
+                                                 (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr, nrows);
+    DK_CUDA(cudaGetLastError());
+    st().launches++;
+    return;
+  }
+  if (kind == "MATVEC" || kind == "SPMV") {
+    if (n != 3) fail(DK_ERR_ARG, "%s expects 3 args", kind.c_str());
+    for (int i = 0; i < 3; ++i) check_f64(v[i], kind.c_str());
+    if (v[0].rank != 2 || v[1].rank != 1 || v[2].rank != 1 || v[0].ext[1] != v[1].ext[0] || v[0].ext[0] != v[2].ext[0])
+      fail(DK_ERR_UNSUPPORTED, "%s: only (m,k) @ (k,) -> (m,) is supported", kind.c_str());
+    const int64_t m = v[0].ext[0];
+    if (m == 0) return;
+    int blocks = (int)std::min<int64_t>((m * 32 + 255) / 256, (int64_t)sms * 8);
+    k_matvec<<<blocks, 256, 0, s>>>(v[0], v[1], v[2]);
+    DK_CUDA(cudaGetLastError());
+    st().launches++;
+    return;
+  }
+  if (kind == "NORM") {
+    if (n != 2) fail(DK_ERR_ARG, "NORM expects 2 args");
+    check_f64(v[0], "NORM");
+    check_f64(v[1], "NORM");
+    k_norm<<<1, 1024, 0, s>>>(v[0], v[1]);
+    DK_CUDA(cudaGetLastError());
+    st().launches++;
+    return;
+  }
+  if (kind == "OPAQUE") {
+    for (int i = 0; i < n; ++i) {
+      if (!writes[i]) continue;
+      check_f64(v[i], "OPAQUE");
+      int64_t cnt = view_volume(v[i]);
+      if (cnt == 0) continue;
+      int blocks = (int)std::min<int64_t>((cnt + 255) / 256, (int64_t)sms * 8);
+      k_add_one<<<blocks, 256, 0, s>>>(v[i]);
+      DK_CUDA(cudaGetLastError());
+      st().launches++;
+    }
+    return;
+  }
+  fail(DK_ERR_STATE, "no builtin for task kind '%s'", kind.c_str());
+}
+
+}  // namespace dk

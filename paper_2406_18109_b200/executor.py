@@ -1,0 +1,686 @@
+"""Task executor of the B200 backend (replaces diffusekit executor.py:163-195).
+
+One process drives one GPU.  With ``world`` processes the launch points of an
+index task are mapped to ranks by their lexicographic ordinal (block
+distribution; one point per GPU when the launch volume equals the world size,
+PAPER.md:1496-1498).  Every rank runs the same front end and therefore sees
+the same stream of launches (replicated control); each rank only executes its
+own points, on stores backed in HBM only where its points touch them.
+
+Coherence.  Per store the executor keeps, identically on every rank, the rects
+each rank holds valid and the rects ever written.  Before a launch it computes
+what each rank's points read (R/RW views, Rd targets, builtin inputs); missing
+rects are fetched from a rank that holds them (grouped NCCL send/recv, same
+plan on every rank so sends and receives pair up) or materialised from the
+store's initial contents if nobody ever wrote them (the Heap's lazy
+initialisation, executor.py:54-61).  Writes invalidate other ranks' copies.
+Fused windows need no data from other points by construction
+(fusion.py:72-122), so exchanges only happen between launches: stencil halo
+rows, replicated (NonePart) reads of tile-written vectors, partial sums.
+
+Reductions.  With one rank every reduce statement accumulates directly into
+its target in point order.  With several, each point's per-statement totals are
+all-gathered and every rank folds ``acc = acc + total_p`` in lexicographic
+point order -- the reference's combine order (executor.py:193-195), so the
+replicated target is bit-identical on all ranks.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_double, c_int, c_int32, c_int64, c_uint8, c_uint64
+from dataclasses import dataclass, field
+from typing import Iterable, Mapping, Sequence
+
+import numpy as np
+
+from . import regions as rg
+from . import runtime
+from .errors import BackendError, UnknownTaskKind, UnsupportedError
+from .initheap import host_contents, poisson_tile, poisson_tile_layout, row_chunks
+from .ir import KProg, TaskDesc, rect_of
+from .runtime import DK_F64, DK_I32, check, dk_view, i64s
+
+BUILTIN_KINDS = ("MATVEC", "SPMV", "NORM", "OPAQUE", "SPMV_CSR")
+
+
+@dataclass
+class StoreRec:
+    sid: int
+    shape: tuple[int, ...]
+    dtype: str  # "f64" | "i32"
+    valid: list[list] = field(default_factory=list)  # per rank: disjoint rects
+    written: list = field(default_factory=list)
+    on_device: bool = False
+    base: int = 0
+    strides: tuple[int, ...] = ()
+
+    @property
+    def esize(self) -> int:
+        return 8 if self.dtype == "f64" else 4
+
+    @property
+    def full(self):
+        return (tuple(0 for _ in self.shape), tuple(self.shape))
+
+
+@dataclass
+class LaunchStats:
+    launches: int = 0
+    points: int = 0
+    bytes_moved: int = 0
+    transfers: int = 0
+    inits: int = 0
+
+
+class Executor:
+    """Device-side heap + launch engine for one rank."""
+
+    def __init__(
+        self,
+        shapes: Mapping[int, Sequence[int]] | None = None,
+        seed: int = 0,
+        init: Mapping[int, dict] | None = None,
+        dtypes: Mapping[int, str] | None = None,
+        rank: int = 0,
+        world: int = 1,
+        device: int | None = None,
+        shape_of=None,
+    ) -> None:
+        self.lib = runtime.load()
+        self.rank = rank
+        self.world = world
+        self.device = rank if device is None else device
+        check(self.lib.dk_init(self.device))
+        self.shapes = {int(s): tuple(v) for s, v in (shapes or {}).items()}
+        self.shape_of = shape_of
+        self.seed = seed
+        self.init = dict(init or {})
+        self.dtypes = dict(dtypes or {})
+        self.stores: dict[int, StoreRec] = {}
+        self._kcache: dict[int, tuple[KProg, int, int]] = {}
+        self._kval: dict[KProg, tuple[int, int]] = {}
+        self._scal: dict[tuple, ctypes.Array] = {}
+        self.stats = LaunchStats()
+        self._comm = False
+
+    # ------------------------------------------------------------------ comm
+    def init_comm(self, unique_id: bytes) -> None:
+        buf = (c_uint8 * 128)(*unique_id)
+        check(self.lib.dk_comm_init(self.rank, self.world, buf))
+        self._comm = True
+
+    def comm_unique_id(self) -> bytes:
+        buf = (c_uint8 * 128)()
+        check(self.lib.dk_comm_unique_id(buf))
+        return bytes(buf)
+
+    # ---------------------------------------------------------------- stores
+    def shape(self, sid: int) -> tuple[int, ...]:
+        s = self.shapes.get(sid)
+        if s is None and self.shape_of is not None:
+            s = tuple(self.shape_of(sid))
+            self.shapes[sid] = s
+        if s is None:
+            raise BackendError(f"unknown store {sid}")
+        return s
+
+    def rec(self, sid: int) -> StoreRec:
+        r = self.stores.get(sid)
+        if r is None:
+            shape = self.shape(sid)
+            strides = [1] * len(shape)
+            for d in range(len(shape) - 2, -1, -1):
+                strides[d] = strides[d + 1] * shape[d + 1]
+            r = StoreRec(sid, shape, self.dtypes.get(sid, "f64"), [[] for _ in range(self.world)], [], strides=tuple(strides))
+            self.stores[sid] = r
+        return r
+
+    def _device(self, r: StoreRec) -> None:
+        if r.on_device:
+            return
+        check(self.lib.dk_store_create(r.sid, len(r.shape), i64s(r.shape), DK_F64 if r.dtype == "f64" else DK_I32))
+        p = c_uint64()
+        check(self.lib.dk_store_ptr(r.sid, byref(p)))
+        r.base = p.value
+        r.on_device = True
+
+    def _ensure(self, r: StoreRec, rect) -> None:
+        if rg.empty(rect):
+            return
+        self._device(r)
+        lo, hi = rg.bbox_flat(r.shape, rect)
+        check(self.lib.dk_store_ensure(r.sid, lo, hi))
+
+    def free(self, sid: int) -> None:
+        r = self.stores.pop(sid, None)
+        if r is not None and r.on_device:
+            check(self.lib.dk_store_free(sid))
+
+    def close(self) -> None:
+        """Release every store this executor created (device state is process-global)."""
+        for sid in list(self.stores):
+            self.free(sid)
+        check(self.lib.dk_sync())
+
+    def materialized(self, sid: int) -> bool:
+        r = self.stores.get(sid)
+        return r is not None and any(r.valid[q] for q in range(self.world))
+
+    # -------------------------------------------------- initial contents
+    def _materialize_init(self, r: StoreRec, rects: list) -> None:
+        """Upload the store's initial contents for ``rects`` on this rank."""
+        rects = [x for x in rects if not rg.empty(x)]
+        if not rects:
+            return
+        for x in rects:
+            self._ensure(r, x)
+        self.stats.inits += len(rects)
+        spec = self.init.get(r.sid)
+        kind = None if spec is None else spec["kind"]
+        np_dtype = np.float64 if r.dtype == "f64" else np.int32
+        if kind in ("zeros", "const", "poisson_invdiag") and r.dtype == "f64":
+            v = {"zeros": 0.0, "poisson_invdiag": 0.25}.get(kind, float(spec.get("value", 0.0)))
+            for x in rects:
+                for a, b in self._flat_runs(r, x):
+                    check(self.lib.dk_store_fill(r.sid, a, b, v))
+            return
+        if kind in ("csr_rowptr", "csr_cols", "csr_vals"):
+            self._materialize_csr(r, spec, rects, np_dtype)
+            return
+        if not r.shape:
+            host = host_contents(spec, self.seed, r.sid, r.shape).astype(np_dtype)
+            check(self.lib.dk_store_upload_rect(r.sid, i64s([0]), i64s([0]), host.ctypes.data))
+            return
+        row = 1
+        for e in r.shape[1:]:
+            row *= e
+        row_end = max(x[1][0] for x in rects)
+        for r0, r1, chunk in row_chunks(spec, self.seed, r.sid, r.shape, row_end):
+            chunk = np.ascontiguousarray(chunk, dtype=np_dtype)
+            base = chunk.ctypes.data - r0 * row * r.esize  # virtual full-store origin
+            for x in rects:
+                lo0, hi0 = max(x[0][0], r0), min(x[1][0], r1)
+                if lo0 >= hi0:
+                    continue
+                lo = (lo0,) + x[0][1:]
+                hi = (hi0,) + x[1][1:]
+                check(self.lib.dk_store_upload_rect(r.sid, i64s(lo), i64s(hi), ctypes.c_void_p(base)))
+            check(self.lib.dk_sync())  # the chunk buffer is reused by the generator
+
+    def _materialize_csr(self, r: StoreRec, spec: dict, rects: list, np_dtype) -> None:
+        nx, ny, k = int(spec["nx"]), int(spec["ny"]), int(spec["k"])
+        lay = poisson_tile_layout(nx, ny, k)
+        which = ("csr_rowptr", "csr_cols", "csr_vals").index(spec["kind"])
+        seg = lay["t"] + 1 if which == 0 else lay["nnz_max"]
+        for p in range(k):
+            tile_rect = ((p * seg,), ((p + 1) * seg,))
+            parts = [rg.intersect(x, tile_rect) for x in rects]
+            parts = [x for x in parts if not rg.empty(x)]
+            if not parts:
+                continue
+            arr = np.ascontiguousarray(poisson_tile(nx, ny, k, p)[which], dtype=np_dtype)
+            base = arr.ctypes.data - p * seg * r.esize
+            for x in parts:
+                check(self.lib.dk_store_upload_rect(r.sid, i64s(x[0]), i64s(x[1]), ctypes.c_void_p(base)))
+            check(self.lib.dk_sync())
+
+    def _flat_runs(self, r: StoreRec, x) -> list[tuple[int, int]]:
+        """Contiguous [a, b) element runs covering rect x (row-major)."""
+        shape = r.shape
+        if not shape:
+            return [(0, 1)]
+        n = len(shape)
+        inner = n - 1
+        while inner > 0 and x[0][inner] == 0 and x[1][inner] == shape[inner]:
+            inner -= 1
+        runs = []
+        outer = [range(x[0][d], x[1][d]) for d in range(inner)]
+        import itertools
+
+        for idx in itertools.product(*outer):
+            a = sum(i * r.strides[d] for d, i in enumerate(idx)) + x[0][inner] * r.strides[inner]
+            b = a + (x[1][inner] - x[0][inner]) * r.strides[inner]
+            runs.append((a, b))
+        return runs
+
+    # ------------------------------------------------------------ coherence
+    def point_rank(self, ordinal: int, volume: int) -> int:
+        if self.world == 1:
+            return 0
+        if volume >= self.world:
+            return ordinal * self.world // volume
+        return ordinal
+
+    def _satisfy(self, need: dict[int, dict[int, list]]) -> None:
+        """Make every rank's needed rects valid (same plan on every rank)."""
+        snap = {sid: [list(v) for v in self.stores[sid].valid] for sid in {s for d in need.values() for s in d}}
+        transfers = []  # (sid, rect, src, dst)
+        inits: dict[int, list] = {}
+        for q in range(self.world):
+            for sid in sorted(need.get(q, {})):
+                r = self.stores[sid]
+                for want in need[q][sid]:
+                    missing = rg.minus([want], r.valid[q])
+                    for m in missing:
+                        unwritten = rg.minus([m], r.written)
+                        if q == self.rank and unwritten:
+                            inits.setdefault(sid, []).extend(unwritten)
+                        rest = rg.minus([m], unwritten)
+                        for src in range(self.world):
+                            if not rest:
+                                break
+                            if src == q:
+                                continue
+                            for v in snap[sid][src]:
+                                for rr in rest:
+                                    piece = rg.intersect(rr, v)
+                                    if not rg.empty(piece):
+                                        transfers.append((sid, piece, src, q))
+                                rest = rg.minus(rest, [v])
+                                if not rest:
+                                    break
+                        if rest:
+                            raise BackendError(f"coherence: store {sid} rect {rest[0]} valid nowhere")
+                    r.valid[q] = rg.add(r.valid[q], want) if missing else r.valid[q]
+        for sid, rects in inits.items():
+            self._materialize_init(self.stores[sid], rects)
+        mine = [t for t in transfers if self.rank in (t[2], t[3])]
+        if mine:
+            if not self._comm:
+                raise BackendError("multi-rank transfer without an initialised communicator")
+            n = len(mine)
+            sids = (c_int64 * n)()
+            peers = (c_int32 * n)()
+            dirs = (c_int32 * n)()
+            los = (c_int64 * (4 * n))()
+            his = (c_int64 * (4 * n))()
+            for i, (sid, rect, src, dst) in enumerate(mine):
+                r = self.stores[sid]
+                self._ensure(r, rect)
+                sids[i] = sid
+                send = src == self.rank
+                peers[i] = dst if send else src
+                dirs[i] = 0 if send else 1
+                for d in range(len(rect[0])):
+                    los[4 * i + d] = rect[0][d]
+                    his[4 * i + d] = rect[1][d]
+                self.stats.bytes_moved += rg.volume(rect) * r.esize
+            self.stats.transfers += n
+            check(self.lib.dk_comm_exchange(n, sids, peers, dirs, los, his))
+
+    def _wrote(self, sid: int, rect, q: int) -> None:
+        r = self.stores[sid]
+        if rg.empty(rect):
+            return
+        for o in range(self.world):
+            if o != q and r.valid[o]:
+                r.valid[o] = rg.minus(r.valid[o], [rect])
+        r.valid[q] = rg.add(r.valid[q], rect)
+        r.written = rg.add(r.written, rect)
+
+    # --------------------------------------------------------------- views
+    def view(self, r: StoreRec, rect) -> dk_view:
+        v = dk_view()
+        lo, hi = rect
+        off = sum(l * s for l, s in zip(lo, r.strides))
+        v.ptr = r.base + off * r.esize
+        v.rank = len(r.shape)
+        v.dtype = DK_F64 if r.dtype == "f64" else DK_I32
+        for d in range(len(r.shape)):
+            v.ext[d] = max(0, hi[d] - lo[d])
+            v.stride[d] = r.strides[d]
+        return v
+
+    # -------------------------------------------------------------- kernels
+    def kernel_handle(self, kp: KProg) -> tuple[int, int]:
+        hit = self._kcache.get(id(kp))
+        if hit is not None and hit[0] is kp:
+            return hit[1], hit[2]
+        val = self._kval.get(kp)
+        if val is None:
+            text = kp.wire([s.decl_rank for s in kp.slots]).encode()
+            h = c_int64()
+            check(self.lib.dk_kernel_compile(text, len(text), byref(h)))
+            nred = sum(1 for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce")
+            val = (h.value, nred)
+            self._kval[kp] = val
+        self._kcache[id(kp)] = (kp, val[0], val[1])
+        return val
+
+    def kernel_source(self, kp: KProg) -> str:
+        h, _ = self.kernel_handle(kp)
+        n = c_int64()
+        check(self.lib.dk_kernel_source(h, None, 0, byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check(self.lib.dk_kernel_source(h, buf, n.value + 1, byref(n)))
+        return buf.value.decode()
+
+    def _scalars(self, vals: tuple[float, ...]) -> ctypes.Array:
+        a = self._scal.get(vals)
+        if a is None:
+            a = (c_double * max(len(vals), 1))(*vals)
+            if len(self._scal) > 4096:
+                self._scal.clear()
+            self._scal[vals] = a
+        return a
+
+    # ------------------------------------------------------------- execute
+    def execute(self, task: TaskDesc, kp: KProg | None, temp_positions: Iterable[int] = ()) -> None:
+        """Run one (fused or plain) index task: execute_task (executor.py:163-195)."""
+        if kp is None and task.kind not in BUILTIN_KINDS:
+            raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
+        temp_positions = frozenset(temp_positions)
+        pts = list(task.points())
+        V = len(pts)
+        prank = [self.point_rank(i, V) for i in range(V)]
+        rects = [[rect_of(self.shape(a.store), a.part, p) for a in task.args] for p in pts]
+        for j, a in enumerate(task.args):
+            if j not in temp_positions:
+                self.rec(a.store)
+
+        # access roles per argument
+        if kp is None:
+            reads = [a.reads or a.reduces or (a.writes and task.kind == "OPAQUE") for a in task.args]
+            writes = [a.writes for a in task.args]
+            reduces = [False] * len(task.args)
+            if task.kind == "NORM":
+                reads = [a.reads or a.reduces for a in task.args]
+        else:
+            stored = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "store"}
+            red_slots = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce"}
+            reads = [False] * len(task.args)
+            writes = [False] * len(task.args)
+            reduces = [False] * len(task.args)
+            for i, s in enumerate(kp.slots):
+                if s.local:
+                    continue
+                a = task.args[s.arg]
+                if a.reads:
+                    reads[s.arg] = True
+                if i in stored and a.writes:
+                    writes[s.arg] = True
+                if i in red_slots:
+                    reduces[s.arg] = True
+        multi = self.world > 1
+
+        # what each rank must hold before the launch
+        need: dict[int, dict[int, list]] = {}
+        for i in range(V):
+            q = prank[i]
+            for j, a in enumerate(task.args):
+                if j in temp_positions:
+                    continue
+                rect = rects[i][j]
+                if rg.empty(rect):
+                    continue
+                if reads[j]:
+                    need.setdefault(q, {}).setdefault(a.store, []).append(rect)
+                if reduces[j]:
+                    if multi and a.part.is_none:
+                        for o in range(self.world):
+                            need.setdefault(o, {}).setdefault(a.store, []).append(rect)
+                    else:
+                        need.setdefault(q, {}).setdefault(a.store, []).append(rect)
+        if multi:
+            self._check_cross_rank(task, prank, rects, reads, writes, temp_positions)
+        self._satisfy(need)
+
+        mine = [i for i in range(V) if prank[i] == self.rank]
+        if kp is None:
+            self._run_builtin(task, pts, mine, rects, writes)
+        else:
+            self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
+        self.stats.launches += 1
+        self.stats.points += len(mine)
+
+        # bookkeeping of the launch's effects (all ranks, all points)
+        for i in range(V):
+            for j, a in enumerate(task.args):
+                if j in temp_positions:
+                    continue
+                if writes[j]:
+                    self._wrote(a.store, rects[i][j], prank[i])
+                if reduces[j] and not (multi and a.part.is_none):
+                    self._wrote(a.store, rects[i][j], prank[i])
+        if multi:
+            for j, a in enumerate(task.args):
+                if reduces[j] and a.part.is_none and j not in temp_positions:
+                    r = self.stores[a.store]
+                    for o in range(self.world):
+                        r.valid[o] = rg.add(r.valid[o], r.full)
+                    r.written = rg.add(r.written, r.full)
+
+    def _check_cross_rank(self, task, prank, rects, reads, writes, temp_positions) -> None:
+        """Points of one launch on different GPUs must not exchange data."""
+        V = len(prank)
+        if len(set(prank)) < 2:
+            return
+        wr = [(prank[i], a.store, rects[i][j]) for i in range(V) for j, a in enumerate(task.args)
+              if writes[j] and j not in temp_positions]
+        if not wr:
+            return
+        for i in range(V):
+            for j, a in enumerate(task.args):
+                if j in temp_positions or not (reads[j] or writes[j]):
+                    continue
+                for q, sid, w in wr:
+                    if q != prank[i] and sid == a.store and rg.overlaps(w, rects[i][j]):
+                        raise UnsupportedError(
+                            f"{task.kind}: points on different GPUs touch store {sid} where another writes"
+                        )
+
+    def _hazards(self, kp: KProg, task: TaskDesc, rects_p, temp_positions) -> None:
+        params = [(i, s) for i, s in enumerate(kp.slots) if not s.local]
+        wslots = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "store"}
+        for i, s in params:
+            if i not in wslots:
+                continue
+            a = task.args[s.arg]
+            for i2, s2 in params:
+                if i2 == i:
+                    continue
+                b = task.args[s2.arg]
+                if b.store == a.store and rg.overlaps(rects_p[s.arg], rects_p[s2.arg]):
+                    raise UnsupportedError(
+                        f"{task.kind}: written view {s.name} overlaps {s2.name} of the same store {a.store}"
+                    )
+
+    def _run_kernel(self, task, kp, mine, prank, rects, temp_positions, reduces) -> None:
+        if len(kp.scalar_names) != len(task.scalars):
+            raise BackendError(
+                f"task {task.kind} carries {len(task.scalars)} scalars, kernel expects {len(kp.scalar_names)}"
+            )
+        h, nred = self.kernel_handle(kp)
+        scal = self._scalars(task.scalars)
+        nslots = len(kp.slots)
+        red_targets = [
+            (st[1], kp.slots[st[1]]) for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce"
+        ]
+        use_totals = self.world > 1 and nred > 0
+        V = len(prank)
+        totals = 0
+        maxp = 0
+        if use_totals:
+            counts = [0] * self.world
+            for q in prank:
+                counts[q] += 1
+            maxp = max(counts)
+            nbytes = 8 * maxp * nred
+            tb = c_uint64()
+            check(self.lib.dk_scratch_alloc(nbytes * (self.world + 1), byref(tb)))
+            totals = tb.value
+            check(self.lib.dk_memset_zero(totals, nbytes * (self.world + 1)))
+        views = (dk_view * nslots)()
+        for slot_in_rank, i in enumerate(mine):
+            rp = rects[i]
+            self._hazards(kp, task, rp, temp_positions)
+            scratch = []
+            for si, s in enumerate(kp.slots):
+                rect = rp[s.arg]
+                if s.local:
+                    ext = tuple(max(0, h2 - l) for l, h2 in zip(*rect))
+                    n = 1
+                    for e in ext:
+                        n *= e
+                    p = c_uint64()
+                    check(self.lib.dk_scratch_alloc(8 * max(n, 1), byref(p)))
+                    check(self.lib.dk_memset_zero(p.value, 8 * max(n, 1)))
+                    scratch.append(p.value)
+                    v = views[si]
+                    v.ptr = p.value
+                    v.rank = len(ext)
+                    v.dtype = DK_F64
+                    st_ = 1
+                    for d in range(len(ext) - 1, -1, -1):
+                        v.ext[d] = ext[d]
+                        v.stride[d] = st_
+                        st_ *= max(ext[d], 1)
+                else:
+                    r = self.stores[task.args[s.arg].store]
+                    self._ensure(r, rect)
+                    views[si] = self.view(r, rect)
+            tot = totals + 8 * nred * (self.rank * maxp + slot_in_rank) if use_totals else 0
+            check(self.lib.dk_launch(h, views, nslots, scal, len(task.scalars), tot))
+            for p in scratch:
+                check(self.lib.dk_scratch_free(p))
+        if use_totals:
+            self._fold(task, kp, prank, rects, red_targets, totals, maxp, nred)
+            check(self.lib.dk_scratch_free(totals))
+
+    def _fold(self, task, kp, prank, rects, red_targets, totals, maxp, nred) -> None:
+        """All-gather per-point totals; fold in lexicographic point order."""
+        V = len(prank)
+        block = maxp * nred
+        gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
+        check(self.lib.dk_comm_allgather_f64(totals + 8 * block * self.rank, gathered, block))
+        slot_of_point = []
+        seen = [0] * self.world
+        for q in prank:
+            slot_of_point.append(seen[q])
+            seen[q] += 1
+        idx = [[(prank[i] * maxp + slot_of_point[i]) * nred + k for k in range(nred)] for i in range(V)]
+        tslots = [sl for sl, _ in red_targets]
+        distinct = len(set(tslots)) == len(tslots)
+        if distinct:
+            for k, (sl, s) in enumerate(red_targets):
+                a = task.args[s.arg]
+                if a.part.is_none:
+                    r = self.stores[a.store]
+                    self._ensure(r, r.full)
+                    tv = self.view(r, r.full)
+                    ks = [idx[i][k] for i in range(V)]
+                    stride = ks[1] - ks[0] if V > 1 else 1
+                    if all(ks[t] == ks[0] + t * stride for t in range(V)):
+                        check(self.lib.dk_accum(byref(tv), gathered, ks[0], stride, V))
+                    else:
+                        for kk in ks:
+                            check(self.lib.dk_accum(byref(tv), gathered, kk, 1, 1))
+                else:
+                    for i in range(V):
+                        if prank[i] != self.rank:
+                            continue
+                        r = self.stores[a.store]
+                        tv = self.view(r, rects[i][s.arg])
+                        check(self.lib.dk_accum(byref(tv), gathered, idx[i][k], 1, 1))
+            return
+        for i in range(V):
+            for k, (sl, s) in enumerate(red_targets):
+                a = task.args[s.arg]
+                if not a.part.is_none and prank[i] != self.rank:
+                    continue
+                r = self.stores[a.store]
+                rect = r.full if a.part.is_none else rects[i][s.arg]
+                self._ensure(r, rect)
+                tv = self.view(r, rect)
+                check(self.lib.dk_accum(byref(tv), gathered, idx[i][k], 1, 1))
+
+    def _run_builtin(self, task, pts, mine, rects, writes) -> None:
+        n = len(task.args)
+        wflags = (c_int32 * max(n, 1))(*[1 if a.writes else 0 for a in task.args])
+        kind = task.kind.encode()
+        if self.world > 1 and any(a.reduces for a in task.args) and len(set(self.point_rank(i, len(pts)) for i in range(len(pts)))) > 1:
+            raise UnsupportedError(f"{task.kind}: reduction builtin across several GPUs")
+        for i in mine:
+            views = (dk_view * max(n, 1))()
+            for j, a in enumerate(task.args):
+                r = self.stores[a.store]
+                self._ensure(r, rects[i][j])
+                views[j] = self.view(r, rects[i][j])
+            check(self.lib.dk_builtin(kind, views, n, wflags))
+
+    # ---------------------------------------------------------- host access
+    def upload(self, sid: int, host: np.ndarray) -> None:
+        """Replace the whole store with ``host`` (every rank holds it valid)."""
+        r = self.rec(sid)
+        np_dtype = np.float64 if r.dtype == "f64" else np.int32
+        a = np.ascontiguousarray(host, dtype=np_dtype)
+        if a.shape != r.shape:
+            raise ValueError(f"store {sid} has shape {r.shape}, got {a.shape}")
+        self._ensure(r, r.full)
+        check(self.lib.dk_store_upload_rect(sid, i64s(r.full[0]), i64s(r.full[1]), a.ctypes.data))
+        check(self.lib.dk_sync())
+        for o in range(self.world):
+            r.valid[o] = [r.full]
+        r.written = [r.full]
+
+    def upload_async(self, sid: int, host: np.ndarray, rect=None) -> None:
+        """Enqueue an H2D copy of ``rect`` from a full-store host array (pinned for overlap)."""
+        r = self.rec(sid)
+        rect = rect or r.full
+        self._ensure(r, rect)
+        check(self.lib.dk_store_upload_rect(sid, i64s(rect[0]), i64s(rect[1]), host.ctypes.data))
+        self._wrote(sid, rect, self.rank)
+
+    def download(self, sid: int, out: np.ndarray | None = None, rect=None) -> np.ndarray | None:
+        """Collective on all ranks: gather ``rect`` of the store to rank 0 and copy it out."""
+        r = self.rec(sid)
+        rect = rect or r.full
+        self._satisfy({0: {sid: [rect]}})
+        if self.rank != 0:
+            return None
+        np_dtype = np.float64 if r.dtype == "f64" else np.int32
+        if out is None:
+            out = np.empty(r.shape, dtype=np_dtype)
+        self._ensure(r, rect)
+        check(self.lib.dk_store_download_rect(sid, i64s(rect[0]), i64s(rect[1]), out.ctypes.data))
+        return out
+
+    def download_local(self, sid: int, out: np.ndarray, rect) -> np.ndarray:
+        """D2H of a rect this rank holds valid (no gather; ``out`` is full-store shaped)."""
+        r = self.rec(sid)
+        if not rg.covered(r.valid[self.rank], rect):
+            raise BackendError(f"store {sid} rect {rect} is not valid on rank {self.rank}")
+        check(self.lib.dk_store_download_rect(sid, i64s(rect[0]), i64s(rect[1]), out.ctypes.data))
+        return out
+
+    def get(self, sid: int) -> np.ndarray | None:
+        a = self.download(sid)
+        if a is None:
+            return None
+        return a.astype(np.float64) if a.dtype != np.float64 else a
+
+    def sync(self) -> None:
+        check(self.lib.dk_sync())
+
+    def launch_count(self) -> int:
+        n = c_int64()
+        check(self.lib.dk_launch_count(byref(n)))
+        return n.value
+
+    def stream(self) -> int:
+        s = c_uint64()
+        check(self.lib.dk_get_stream(byref(s)))
+        return s.value
+
+    def set_stream(self, ptr: int) -> None:
+        check(self.lib.dk_set_stream(ptr))
+
+
+def replay(ex: Executor, events, on_free=True) -> None:
+    """Drive the executor with recorded plan events (plan.PlanTrace.events)."""
+    for kind, ev in events:
+        if kind == "exec":
+            ex.execute(ev.task, ev.kernel, ev.temp_positions)
+        elif kind == "free" and on_free:
+            ex.free(ev)

@@ -60,6 +60,50 @@ def poisson_tile(nx: int, ny: int, k: int, p: int, dtype_idx=np.float64):
     return rowptr.astype(dtype_idx), c.astype(dtype_idx), v
 
 
+def row_chunks(spec: dict | None, seed: int, sid: int, shape: Sequence[int], row_end: int, chunk_elems: int = 1 << 24):
+    """Yield ``(row0, row1, rows)`` of the initial contents, dim-0 rows ``[0, row_end)``.
+
+    The RNG kinds are generated as one sequential stream in bounded chunks
+    (numpy's Generator continues its stream across calls, so the chunks
+    concatenate to exactly ``host_contents``).  Rank-0 stores yield one chunk.
+    """
+    shape = tuple(shape)
+    if not shape:
+        yield 0, 1, host_contents(spec, seed, sid, shape)
+        return
+    row = 1
+    for e in shape[1:]:
+        row *= e
+    step = max(1, chunk_elems // max(row, 1))
+    kind = None if spec is None else spec["kind"]
+    if kind is None or kind == "uniform":
+        if kind is None:
+            rng = np.random.default_rng([seed, sid])
+            draw = lambda n: rng.integers(1, 10, size=n).astype(np.float64)  # noqa: E731
+        else:
+            rng = np.random.default_rng([int(spec.get("seed", 0)), int(spec.get("key", sid))])
+            scale = float(spec["scale"]) if "scale" in spec else None
+
+            def draw(n):
+                a = rng.random(size=n, dtype=np.float64)
+                if scale is not None:
+                    a *= scale
+                return a
+
+        for r0 in range(0, row_end, step):
+            r1 = min(row_end, r0 + step)
+            yield r0, r1, draw((r1 - r0) * row).reshape((r1 - r0,) + shape[1:])
+        return
+    if kind in ("zeros", "const", "poisson_invdiag"):
+        v = {"zeros": 0.0, "poisson_invdiag": 0.25}.get(kind, float(spec.get("value", 0.0)))
+        for r0 in range(0, row_end, step):
+            r1 = min(row_end, r0 + step)
+            yield r0, r1, np.full((r1 - r0,) + shape[1:], v, dtype=np.float64)
+        return
+    full = host_contents(spec, seed, sid, shape)
+    yield 0, row_end, full[:row_end]
+
+
 def host_contents(spec: dict | None, seed: int, sid: int, shape: Sequence[int]) -> np.ndarray:
     """float64 host array for store ``sid`` under an init spec (None = default rule)."""
     shape = tuple(shape)

@@ -1,0 +1,137 @@
+"""Drop-in ``Session`` whose execution runs on B200 (requires ``diffusekit``).
+
+``GpuSession`` subclasses the reference ``Session`` (pipeline.py:128-373) and
+overrides only what the north star changes:
+
+* ``_execute`` (pipeline.py:312-345): identical report bookkeeping (prefix,
+  temporaries, static traffic, kernel stats), then the fused or plain task is
+  lowered once per ``Kernel`` object and handed to the device executor;
+* ``heap`` (pipeline.py:141): a :class:`GpuHeap` with the reference Heap API
+  (executor.py:40-79) over device stores;
+* ``_maybe_free`` (pipeline.py:371-373) is inherited and reaches
+  ``GpuHeap.free`` -> stream-ordered release.
+
+The front end -- windowing, fusion constraints, temporaries, memoization,
+kernel composition -- is the reference's, untouched.
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+
+from .errors import BoundsError, PrivilegeError, UnknownTaskKind
+from .executor import BUILTIN_KINDS, Executor
+from .ir import lower_kernel, lower_task
+
+from diffusekit import executor as _ref_exec  # noqa: E402  (the reference front end is required here)
+from diffusekit import kernels as _ref_kernels  # noqa: E402
+from diffusekit.pipeline import Session as _RefSession  # noqa: E402
+
+
+class _Arrays:
+    """``Heap.arrays`` look-alike: item assignment uploads (test_executor.py:89-91)."""
+
+    def __init__(self, heap: "GpuHeap") -> None:
+        self._heap = heap
+
+    def __setitem__(self, sid: int, value) -> None:
+        a = np.asarray(value, dtype=np.float64)
+        self._heap.ex.upload(sid, a)
+
+    def __getitem__(self, sid: int) -> np.ndarray:
+        if not self._heap.materialized(sid):
+            raise KeyError(sid)
+        return self._heap.get(sid)
+
+    def __contains__(self, sid: int) -> bool:
+        return self._heap.materialized(sid)
+
+    def pop(self, sid: int, default=None):
+        if sid in self:
+            v = self[sid]
+            self._heap.free(sid)
+            return v
+        return default
+
+
+class GpuHeap:
+    """Reference ``Heap`` API over device-resident stores."""
+
+    def __init__(self, executor: Executor) -> None:
+        self.ex = executor
+        self.arrays = _Arrays(self)
+
+    def get(self, store_id: int) -> np.ndarray:
+        return self.ex.get(store_id)
+
+    def materialized(self, store_id: int) -> bool:
+        return self.ex.materialized(store_id)
+
+    def free(self, store_id: int) -> None:
+        self.ex.free(store_id)
+
+    def digest(self, ids: Sequence[int]) -> dict[int, bytes]:
+        return {s: self.get(s).tobytes() for s in ids}
+
+    def dump_text(self, ids: Sequence[int]) -> str:
+        lines = []
+        for s in sorted(ids):
+            arr = self.get(s)
+            lines.append(f"store {s} shape {arr.shape}:")
+            lines.append(np.array2string(arr, precision=6))
+        return "\n".join(lines)
+
+
+class GpuSession(_RefSession):
+    def __init__(self, config=None, registry=None, builtins=None, *, rank=0, world=1, device=None,
+                 init=None, dtypes=None):
+        super().__init__(config, registry, builtins)
+        self.executor = Executor(
+            seed=self.config.seed,
+            init=init,
+            dtypes=dtypes,
+            rank=rank,
+            world=world,
+            device=device,
+            shape_of=lambda sid: self.stores[sid].shape.extents,
+        )
+        self.heap = GpuHeap(self.executor)
+        self._lowered: dict[int, tuple[object, object]] = {}
+
+    def _lower(self, kernel, fused: bool):
+        hit = self._lowered.get(id(kernel))
+        if hit is not None and hit[0] is kernel:
+            return hit[1]
+        kp = lower_kernel(kernel, fused)
+        self._lowered[id(kernel)] = (kernel, kp)
+        return kp
+
+    def _execute(self, plan, fr) -> None:  # pipeline.py:312-345
+        fr.fused_prefixes.append(plan.f)
+        fr.temporaries.extend(sorted(plan.temp_stores))
+        kernel = plan.kernel
+        names_fused = kernel is not None
+        if kernel is None and self.registry.has(plan.task.kind):
+            kernel = self.registry.generate(plan.task)
+        if kernel is not None:
+            loads, stores = self._traffic(kernel, plan.task, plan.temp_positions, names_fused)
+            fr.loads += loads
+            fr.stores += stores
+            fr.kernel_stats.append((plan.f, len(kernel.nests), len(kernel.locals)))
+        if self.config.execute:
+            if kernel is None and (plan.task.kind not in self.builtins or plan.task.kind not in BUILTIN_KINDS):
+                raise _ref_exec.UnknownTaskKindError(
+                    f"no generator or device builtin for task kind {plan.task.kind!r}"
+                )
+            kp = self._lower(kernel, names_fused) if kernel is not None else None
+            try:
+                self.executor.execute(lower_task(plan.task), kp, plan.temp_positions)
+            except UnknownTaskKind as e:
+                raise _ref_exec.UnknownTaskKindError(str(e)) from e
+            except PrivilegeError as e:
+                raise _ref_kernels.PrivilegeViolationError(str(e)) from e
+            except BoundsError as e:
+                raise _ref_kernels.OutOfBoundsError(str(e)) from e
+        fr.tasks_out += 1
