@@ -263,7 +263,7 @@ static bool bcast_strides(const dk_view& v, const int64_t* D, int r, int64_t* ou
     if (jj < 0) {
       out[j] = 0;
     } else if (v.ext[jj] == D[j]) {
-      out[j] = D[j] == 1 ? 0 : v.stride[jj];
+      out[j] = v.stride[jj];  // extent-1 dims keep their (irrelevant) stride: innermost stays contiguous
     } else if (v.ext[jj] == 1) {
       out[j] = 0;
     } else {
@@ -408,8 +408,14 @@ __device__ __forceinline__ double dk_max(double a, double b) { return dk_isnan(a
 __device__ __forceinline__ double dk_lt(double a, double b) { return a < b ? 1.0 : 0.0; }
 __device__ __forceinline__ double dk_le(double a, double b) { return a <= b ? 1.0 : 0.0; }
 __device__ __forceinline__ double dk_eq(double a, double b) { return a == b ? 1.0 : 0.0; }
+// np.negative flips the sign bit, NaN payload included.  Plain C (-a or an
+// integer xor) is turned into DADD -RZ, -a by ptxas, which canonicalises NaN;
+// an opaque PTX xor on the high word keeps the bit pattern.
 __device__ __forceinline__ double dk_neg(double a) {
-  return __longlong_as_double(__double_as_longlong(a) ^ (long long)0x8000000000000000ULL);
+  double r;
+  asm("{ .reg .b32 lo, hi; mov.b64 {lo, hi}, %1; xor.b32 hi, hi, 0x80000000; mov.b64 %0, {lo, hi}; }"
+               : "=d"(r) : "d"(a));
+  return r;
 }
 __device__ __forceinline__ double dk_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 

@@ -58,9 +58,15 @@ class PlanTrace:
             out[-1].append(ev)
             if ev[0] == "flush" and ev[1]:
                 out.append([])
-        if not out[-1]:
-            out.pop()
-        return out
+        # a trailing flush of an empty buffer (Session.finish) carries no work;
+        # fold exec-less groups into their predecessor so frees are not lost
+        merged: list[list[tuple[str, Any]]] = []
+        for g in out:
+            if merged and not any(k == "exec" for k, _ in g):
+                merged[-1].extend(g)
+            else:
+                merged.append(g)
+        return [g for g in merged if g]
 
     # ---- serialisation ---------------------------------------------------
 
