@@ -94,8 +94,8 @@ int dk_kernel_source(int64_t handle, char* buf, int64_t cap, int64_t* len);
 int dk_kernel_num_reductions(int64_t handle, int* n);
 /* Device-free code generation (and optional NVRTC compile) for a binding:
  * returns the generated CUDA source.  Used by the CPU test-suite. */
-int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews, int compile,
-                      char* buf, int64_t cap, int64_t* out_len);
+int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews,
+                      const double* scalars, int compile, char* buf, int64_t cap, int64_t* out_len);
 
 /* Run one launch point.  views[i] binds slot i.  totals == 0: every reduce
  * statement accumulates into its target view in statement order; otherwise

@@ -311,6 +311,15 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
                slot, v.rank, r);
         int64_t inner = r ? str[r - 1] : 0;
         s.cls = inner == 1 ? 'C' : inner == 0 ? 'B' : 'G';
+        if (s.cls == 'C') {
+          // 'A': every row's element pairs are 16-byte aligned -> LDG.E.128 / STG.E.128
+          int64_t shift = 0;
+          for (size_t d = 0; d < o.size(); ++d) shift += o[d] * v.stride[d];
+          bool al = ((v.ptr + 8ull * (uint64_t)shift) % 16) == 0;
+          for (int d = 0; d + 1 < r; ++d)
+            if (str[d] % 2) al = false;
+          if (al) s.cls = 'A';
+        }
       }
       if (!o.empty()) {
         if ((int)o.size() != r || v.rank != r)
@@ -419,27 +428,31 @@ __device__ __forceinline__ double dk_neg(double a) {
 }
 __device__ __forceinline__ double dk_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 
-__device__ __forceinline__ double2 dk_ldp(const DkSite& s, int64_t ro, int64_t e, bool full) {
-  const double* p = (const double*)s.p + ro;
-  double2 v;
-  if (s.mode == 0) {
-    if (full) return *reinterpret_cast<const double2*>(p + e);
-    v.x = p[e]; v.y = 0.0; return v;
-  }
-  if (s.mode == 1) { v.x = p[e]; v.y = full ? p[e + 1] : 0.0; return v; }
-  if (s.mode == 2) { v.x = p[0]; v.y = v.x; return v; }
-  v.x = p[e * s.sti]; v.y = full ? p[(e + 1) * s.sti] : 0.0; return v;
+// element-pair access, specialised per site class at code generation time:
+//   A aligned contiguous (one 16-byte access), C contiguous (two 8-byte),
+//   B broadcast inner dim (one load), G strided inner dim
+__device__ __forceinline__ double2 dk_ld_A(const double* p, int64_t e, bool full) {
+  if (full) return *reinterpret_cast<const double2*>(p + e);
+  double2 v; v.x = p[e]; v.y = 0.0; return v;
 }
-
-__device__ __forceinline__ void dk_stp(const DkSite& s, int64_t ro, int64_t e, bool full, double x, double y) {
-  double* p = (double*)s.p + ro;
-  if (s.mode == 0) {
-    if (full) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; }
-    else p[e] = x;
-    return;
-  }
-  if (s.mode == 1) { p[e] = x; if (full) p[e + 1] = y; return; }
-  p[e * s.sti] = x; if (full) p[(e + 1) * s.sti] = y;
+__device__ __forceinline__ double2 dk_ld_C(const double* p, int64_t e, bool full) {
+  double2 v; v.x = p[e]; v.y = full ? p[e + 1] : 0.0; return v;
+}
+__device__ __forceinline__ double2 dk_ld_B(const double* p, int64_t, bool) {
+  double2 v; v.x = p[0]; v.y = v.x; return v;
+}
+__device__ __forceinline__ double2 dk_ld_G(const double* p, int64_t e, bool full, int64_t s) {
+  double2 v; v.x = p[e * s]; v.y = full ? p[(e + 1) * s] : 0.0; return v;
+}
+__device__ __forceinline__ void dk_st_A(double* p, int64_t e, bool full, double x, double y) {
+  if (full) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; }
+  else p[e] = x;
+}
+__device__ __forceinline__ void dk_st_C(double* p, int64_t e, bool full, double x, double y) {
+  p[e] = x; if (full) p[e + 1] = y;
+}
+__device__ __forceinline__ void dk_st_G(double* p, int64_t e, bool full, double x, double y, int64_t s) {
+  p[e * s] = x; if (full) p[(e + 1) * s] = y;
 }
 
 __device__ __forceinline__ double dk_warp_sum(double v) {
@@ -453,7 +466,7 @@ __device__ __forceinline__ double dk_ldcg(const double* p) {
   return v;
 }
 
-__device__ void dk_view_add(const dk_view& t, double v) {
+__device__ __forceinline__ void dk_view_add(const dk_view& t, double v) {
   int64_t n = 1;
   for (int d = 0; d < t.rank; ++d) n *= t.ext[d];
   double* p = (double*)t.ptr;
@@ -465,12 +478,40 @@ __device__ void dk_view_add(const dk_view& t, double v) {
 }
 )DK";
 
-static const int kUnroll = 2;
 static const int kTPB = 256;
+
+// Streaming fused nests are latency-bound unless enough bytes are in flight:
+// ~1.5 us of HBM latency x 6.5 TB/s needs ~64 KB outstanding per SM.  The
+// default asks ptxas for 4 resident 256-thread CTAs per SM (<= 64 registers)
+// with 2 element pairs per thread in flight per operand; modules that would
+// spill at that budget are regenerated with 2 and then 1 CTA per SM.
+struct GenOpts {
+  int unroll = 2;
+  int min_blocks = 4;
+};
+
+static GenOpts default_opts(const std::vector<NestPlan>& plans) {
+  GenOpts o;
+  // many-operand nests (the stencil's five views) keep one pair per operand in
+  // flight; their bytes in flight per thread are already 5 x 16 B
+  size_t most = 0;
+  for (const NestPlan& np : plans) {
+    size_t n = 0;
+    for (size_t i = 0; i < np.sites.size(); ++i) n += np.sites[i].cls != 'S' && np.site_loaded[i];
+    most = std::max(most, n);
+  }
+  o.unroll = most <= 3 ? 2 : 1;
+  if (const char* u = getenv("DK_JIT_UNROLL")) o.unroll = std::max(1, atoi(u));
+  if (const char* m = getenv("DK_JIT_MINB")) o.min_blocks = std::max(1, atoi(m));
+  return o;
+}
 
 class Gen {
  public:
-  Gen(const Prog& g, const std::vector<NestPlan>& plans) : g_(g), plans_(plans) {}
+  Gen(const Prog& g, const std::vector<NestPlan>& plans, const std::string& name = "dk", GenOpts opts = GenOpts(),
+      std::vector<int> scalar_rep = {})
+      : g_(g), plans_(plans), name_(name), kUnroll(opts.unroll), minb_(opts.min_blocks),
+        opts_rep_(std::move(scalar_rep)) {}
 
   std::string source() {
     std::ostringstream o;
@@ -482,6 +523,10 @@ class Gen {
  private:
   const Prog& g_;
   const std::vector<NestPlan>& plans_;
+  std::string name_;
+  int kUnroll;
+  int minb_;
+  std::vector<int> opts_rep_;
 
   int site_index(const NestPlan& np, int slot, const std::vector<int64_t>& offs) const {
     std::vector<int64_t> o = nonzero(offs) ? offs : std::vector<int64_t>();
@@ -517,7 +562,9 @@ class Gen {
         return "v" + std::to_string(si) + "[u]." + lane;
       }
       case 'P':
-        return "P.sc[" + std::to_string(e.i) + "]";
+        // scalars equal to an earlier one (bitwise) read that one: ptxas keeps one
+        // register per distinct value instead of one per task scalar
+        return "P.sc[" + std::to_string(e.i < (int)opts_rep_.size() ? opts_rep_[e.i] : e.i) + "]";
       case 'C':
         snprintf(buf, sizeof buf, "dk_bits(0x%016llxULL)", (unsigned long long)e.bits);
         return buf;
@@ -542,7 +589,8 @@ class Gen {
     const int NR = (int)np.red_slots.size();
     o << "\nstruct P" << n << " { DkHdr h; DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ") dk_n" << n << "(const P" << n << " P) {\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_ << "_n" << n
+      << "(const P" << n << " P) {\n";
     // hoisted rank-0 operands
     for (int i = 0; i < NS; ++i)
       if (np.sites[i].cls == 'S') o << "  const double S" << i << " = *(const double*)P.s[" << i << "].p;\n";
@@ -566,7 +614,9 @@ class Gen {
     o << "  const int TX = blockDim.x;\n";
     o << "  for (int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; row < nrows; row += (int64_t)gridDim.y * blockDim.y) {\n";
     // outer indices of this row
-    if (r >= 2) {
+    if (r == 2) {
+      o << "    const int64_t oi[1] = {row};\n";
+    } else if (r > 2) {
       o << "    int64_t oi[3] = {0, 0, 0};\n";
       o << "    { int64_t rem = row;\n";
       for (int d = r - 2; d >= 0; --d) o << "      oi[" << d << "] = rem % P.h.ext[" << d << "]; rem /= P.h.ext[" << d << "];\n";
@@ -574,7 +624,7 @@ class Gen {
     }
     for (int i = 0; i < NS; ++i) {
       if (np.sites[i].cls == 'S') continue;
-      o << "    const int64_t ro" << i << " = 0";
+      o << "    double* const b" << i << " = (double*)P.s[" << i << "].p";
       for (int d = 0; d < r - 1; ++d) o << " + oi[" << d << "] * P.s[" << i << "].st[" << d << "]";
       o << ";\n";
     }
@@ -589,7 +639,10 @@ class Gen {
     o << "        if (q < npairs) {\n          const int64_t e = 2 * q; const bool full = e + 1 < ninner;\n";
     for (int i = 0; i < NS; ++i) {
       if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
-      o << "          v" << i << "[u] = dk_ldp(P.s[" << i << "], ro" << i << ", e, full);\n";
+      const char c = np.sites[i].cls;
+      o << "          v" << i << "[u] = dk_ld_" << c << "(b" << i << ", e, full";
+      if (c == 'G') o << ", P.s[" << i << "].sti";
+      o << ");\n";
     }
     o << "        }\n      }\n";
     // phase 2: compute + store
@@ -601,7 +654,10 @@ class Gen {
     o << "        if (full) {\n" << lane_code(np, ne, "y") << "        }\n";
     for (int w : wslots) {
       int si = site_index(np, w, {});
-      o << "        dk_stp(P.s[" << si << "], ro" << si << ", e, full, w" << w << "_x, w" << w << "_y);\n";
+      const char c = np.sites[si].cls;
+      o << "        dk_st_" << c << "(b" << si << ", e, full, w" << w << "_x, w" << w << "_y";
+      if (c == 'G') o << ", P.s[" << si << "].sti";
+      o << ");\n";
     }
     o << "        }\n      }\n";
     o << "    }\n  }\n";
@@ -723,7 +779,7 @@ class Gen {
     o << "  if (!dk_last) return;\n  __threadfence();\n";
     o << "  double dk_tot[" << NA << "];\n";
     for (int a = 0; a < np.n_array_red; ++a) {
-      o << "  { double s = 0.0; for (int64_t i = lin; i < G; i += 256) s = dk_add(s, dk_ldcg(red_part + " << a
+      o << "  { double s = 0.0;\n    #pragma unroll 1\n    for (int64_t i = lin; i < G; i += 256) s = dk_add(s, dk_ldcg(red_part + " << a
         << " * G + i)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0) dk_sred[" << a << "][wid] = s; }\n";
     }
     o << "  __syncthreads();\n";
@@ -811,6 +867,7 @@ struct Module {
   std::vector<double*> red_part;
   std::vector<unsigned int*> ticket;
   std::string src;
+  int unroll = 2;
 };
 
 struct KernelObj {
@@ -822,23 +879,53 @@ struct KernelObj {
 
 static std::vector<std::unique_ptr<KernelObj>> g_kernels;
 
-static Module* get_module(KernelObj& k, const dk_view* views) {
+static Module* get_module(KernelObj& k, const dk_view* views, const double* scalars) {
   std::string key;
   std::vector<NestPlan> plans = plan_nests(k.prog, views, &key);
+  // bitwise-equal scalar classes are part of the binding class
+  std::vector<int> rep(k.prog.nscal);
+  for (int i = 0; i < k.prog.nscal; ++i) {
+    rep[i] = i;
+    for (int j = 0; j < i; ++j)
+      if (memcmp(&scalars[i], &scalars[j], 8) == 0) {
+        rep[i] = rep[j];
+        break;
+      }
+    key += "s" + std::to_string(rep[i]);
+  }
   auto it = k.mods.find(key);
   if (it != k.mods.end()) return it->second.get();
   auto m = std::make_unique<Module>();
-  Gen gen(k.prog, plans);
-  m->src = gen.source();
-  k.last_src = m->src;
-  std::string log;
-  std::string bin = compile_cubin(m->src, &log);
-  DK_CU(cuModuleLoadData(&m->mod, bin.data()));
+  char name[32];
+  snprintf(name, sizeof name, "dkf_%08llx", (unsigned long long)(fnv1a(k.text) & 0xffffffffull));
+  GenOpts opts = default_opts(plans);
+  std::vector<CUfunction> fns;
+  for (;;) {
+    Gen gen(k.prog, plans, name, opts, rep);
+    m->src = gen.source();
+    k.last_src = m->src;
+    std::string log;
+    std::string bin = compile_cubin(m->src, &log);
+    DK_CU(cuModuleLoadData(&m->mod, bin.data()));
+    fns.clear();
+    bool spills = false;
+    for (size_t n = 0; n < k.prog.nests.size(); ++n) {
+      CUfunction f;
+      std::string nm = std::string(name) + "_n" + std::to_string(n);
+      DK_CU(cuModuleGetFunction(&f, m->mod, nm.c_str()));
+      int local = 0;
+      DK_CU(cuFuncGetAttribute(&local, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f));
+      spills |= local > 0;
+      fns.push_back(f);
+    }
+    if (!spills || opts.min_blocks == 1) break;
+    DK_CU(cuModuleUnload(m->mod));
+    opts.min_blocks = opts.min_blocks > 2 ? 2 : 1;
+  }
+  m->unroll = opts.unroll;
   const int sms = st().sm_count;
   for (size_t n = 0; n < k.prog.nests.size(); ++n) {
-    CUfunction f;
-    std::string nm = "dk_n" + std::to_string(n);
-    DK_CU(cuModuleGetFunction(&f, m->mod, nm.c_str()));
+    CUfunction f = fns[n];
     int occ = 1;
     DK_CU(cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kTPB, 0));
     occ = std::max(occ, 1);
@@ -871,7 +958,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   const Prog& g = k.prog;
   if (nviews != g.nslots) fail(DK_ERR_ARG, "launch binds %d views, kernel has %d slots", nviews, g.nslots);
   if (nscal != g.nscal) fail(DK_ERR_ARG, "launch passes %d scalars, kernel expects %d", nscal, g.nscal);
-  Module* m = get_module(k, views);
+  Module* m = get_module(k, views, scalars);
   State& S = st();
   int kbase = 0;
   std::vector<char> blob;
@@ -908,16 +995,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       o.p = v.ptr + 8ull * (uint64_t)shift;
       for (int d = 0; d < 3 && d + 1 < r; ++d) o.st[d] = str[d];
       o.sti = r ? str[r - 1] : 0;
-      if (s.cls == 'S' || s.cls == 'B') {
-        o.mode = 2;
-      } else if (s.cls == 'G') {
-        o.mode = 3;
-      } else {
-        bool al = (o.p % 16) == 0;
-        for (int d = 0; d + 1 < r; ++d)
-          if (str[d] % 2) al = false;
-        o.mode = al ? 0 : 1;
-      }
+      o.mode = s.cls == 'A' ? 0 : s.cls == 'C' ? 1 : s.cls == 'G' ? 3 : 2;  // informational: code is specialised
     }
     std::vector<dk_view> rd(std::max(NR, 1));
     memset(rd.data(), 0, sizeof(dk_view) * rd.size());
@@ -939,7 +1017,8 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       tx = (unsigned)(npairs >= kTPB ? kTPB : std::max<int64_t>(32, pow2ceil(npairs)));
       ty = kTPB / tx;
       const int64_t maxg = (int64_t)S.sm_count * m->occ[n];
-      int64_t GX = std::min<int64_t>((npairs + (int64_t)tx * kUnroll - 1) / ((int64_t)tx * kUnroll), maxg);
+      const int64_t U = m->unroll;
+      int64_t GX = std::min<int64_t>((npairs + (int64_t)tx * U - 1) / ((int64_t)tx * U), maxg);
       GX = std::max<int64_t>(GX, 1);
       int64_t GY = std::min<int64_t>((h.nrows + ty - 1) / ty, std::max<int64_t>(1, maxg / GX));
       GY = std::min<int64_t>(std::max<int64_t>(GY, 1), 65535);
@@ -992,14 +1071,23 @@ int dk_kernel_source(int64_t handle, char* buf, int64_t cap, int64_t* len) {
   });
 }
 
-int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews, int compile, char* buf,
-                      int64_t cap, int64_t* out_len) {
+int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews, const double* scalars,
+                      int compile, char* buf, int64_t cap, int64_t* out_len) {
   return guard([&] {
     Prog g = parse_prog(std::string(program, (size_t)len));
     if (nviews != g.nslots) fail(DK_ERR_ARG, "codegen binds %d views, kernel has %d slots", nviews, g.nslots);
     std::string key;
     std::vector<NestPlan> plans = plan_nests(g, views, &key);
-    Gen gen(g, plans);
+    std::vector<int> rep(g.nscal);
+    for (int i = 0; i < g.nscal; ++i) {
+      rep[i] = i;
+      for (int j = 0; scalars && j < i; ++j)
+        if (memcmp(&scalars[i], &scalars[j], 8) == 0) {
+          rep[i] = rep[j];
+          break;
+        }
+    }
+    Gen gen(g, plans, "dk", default_opts(plans), rep);
     std::string src = gen.source();
     if (compile) {
       std::string log;

@@ -68,7 +68,7 @@ _SIGS = {
     "dk_kernel_num_reductions": (c_int, [c_int64, POINTER(c_int)]),
     "dk_kernel_codegen": (
         c_int,
-        [c_char_p, c_int64, POINTER(dk_view), c_int, c_int, c_char_p, c_int64, POINTER(c_int64)],
+        [c_char_p, c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_char_p, c_int64, POINTER(c_int64)],
     ),
     "dk_launch": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_uint64]),
     "dk_accum": (c_int, [POINTER(dk_view), c_uint64, c_int64, c_int64, c_int]),

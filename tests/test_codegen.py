@@ -45,12 +45,14 @@ def views_for(rt, task, kp, shapes, point=None):
     return views
 
 
-def codegen(rt, kp, views, compile_=True):
+def codegen(rt, kp, views, compile_=True, scalars=()):
     text = kp.wire([s.decl_rank for s in kp.slots]).encode()
     n = ctypes.c_int64()
-    rt.check(rt._lib.dk_kernel_codegen(text, len(text), views, len(kp.slots), 1 if compile_ else 0, None, 0, ctypes.byref(n)))
+    sc = (ctypes.c_double * max(len(scalars), 1))(*scalars) if scalars else None
+    rt.check(rt._lib.dk_kernel_codegen(text, len(text), views, len(kp.slots), sc, 1 if compile_ else 0, None, 0,
+                                       ctypes.byref(n)))
     buf = ctypes.create_string_buffer(n.value + 1)
-    rt.check(rt._lib.dk_kernel_codegen(text, len(text), views, len(kp.slots), 0, buf, n.value + 1, ctypes.byref(n)))
+    rt.check(rt._lib.dk_kernel_codegen(text, len(text), views, len(kp.slots), sc, 0, buf, n.value + 1, ctypes.byref(n)))
     return buf.value.decode()
 
 
