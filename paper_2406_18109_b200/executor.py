@@ -38,7 +38,7 @@ from . import regions as rg
 from . import runtime
 from .errors import BackendError, UnknownTaskKind, UnsupportedError
 from .initheap import host_contents, poisson_tile, poisson_tile_layout, row_chunks
-from .ir import KProg, TaskDesc, rect_of
+from .ir import KProg, TaskDesc, rect_of, slot_access
 from .runtime import DK_F64, DK_I32, check, dk_view, i64s
 
 BUILTIN_KINDS = ("MATVEC", "SPMV", "NORM", "OPAQUE", "SPMV_CSR")
@@ -86,8 +86,11 @@ class Executor:
         world: int = 1,
         device: int | None = None,
         shape_of=None,
+        lib=None,
     ) -> None:
-        self.lib = runtime.load()
+        # ``lib``: an object with the C-ABI's functions; only the test-suite's CPU
+        # stand-in passes one.  The product always loads libdk_b200.so.
+        self.lib = lib if lib is not None else runtime.load()
         self.rank = rank
         self.world = world
         self.device = rank if device is None else device
@@ -101,6 +104,7 @@ class Executor:
         self._kcache: dict[int, tuple[KProg, int, int]] = {}
         self._kval: dict[KProg, tuple[int, int]] = {}
         self._scal: dict[tuple, ctypes.Array] = {}
+        self._acc: dict[int, tuple] = {}
         self.stats = LaunchStats()
         self._comm = False
 
@@ -387,8 +391,7 @@ class Executor:
             if task.kind == "NORM":
                 reads = [a.reads or a.reduces for a in task.args]
         else:
-            stored = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "store"}
-            red_slots = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce"}
+            read_first, stored, red_slots = self._access(kp)
             reads = [False] * len(task.args)
             writes = [False] * len(task.args)
             reduces = [False] * len(task.args)
@@ -396,7 +399,7 @@ class Executor:
                 if s.local:
                     continue
                 a = task.args[s.arg]
-                if a.reads:
+                if i in read_first:
                     reads[s.arg] = True
                 if i in stored and a.writes:
                     writes[s.arg] = True
@@ -450,6 +453,13 @@ class Executor:
                     for o in range(self.world):
                         r.valid[o] = rg.add(r.valid[o], r.full)
                     r.written = rg.add(r.written, r.full)
+
+    def _access(self, kp: KProg):
+        hit = self._acc.get(id(kp))
+        if hit is None or hit[0] is not kp:
+            hit = (kp, slot_access(kp))
+            self._acc[id(kp)] = hit
+        return hit[1]
 
     def _check_cross_rank(self, task, prank, rects, reads, writes, temp_positions) -> None:
         """Points of one launch on different GPUs must not exchange data."""

@@ -332,6 +332,45 @@ def stmt_expr(st: tuple) -> tuple:
     return st[3] if st[0] == "store" else st[2]
 
 
+def slot_access(kp: KProg) -> tuple[set[int], set[int], set[int]]:
+    """(read_first, stored, reduced) slots of a kernel.
+
+    ``read_first``: slots whose old contents the kernel observes -- a load that
+    precedes (in nest, then statement order) every store to the slot.  A store
+    covers its whole view (the JIT requires target extents == nest domain), so
+    a slot written before it is read needs no prior contents: no HBM read, no
+    initialisation, no transfer.  Loads in a later nest of a slot stored by an
+    earlier nest read HBM but see this launch's own values, not older ones.
+    """
+    read_first: set[int] = set()
+    stored: set[int] = set()
+    reduced: set[int] = set()
+    for _dom, _rank, stmts in kp.nests:
+        for st in stmts:
+            for slot, _offs in expr_slots(stmt_expr(st)):
+                if slot not in stored:
+                    read_first.add(slot)
+            if st[0] == "store":
+                stored.add(st[1])
+            elif st[0] == "reduce":
+                reduced.add(st[1])
+    return read_first, stored, reduced
+
+
+def hbm_reads(kp: KProg) -> set[int]:
+    """Slots the kernel loads from HBM: per nest, loaded before stored in that nest."""
+    out: set[int] = set()
+    for _dom, _rank, stmts in kp.nests:
+        stored_here: set[int] = set()
+        for st in stmts:
+            for slot, _offs in expr_slots(stmt_expr(st)):
+                if slot not in stored_here:
+                    out.add(slot)
+            if st[0] == "store":
+                stored_here.add(st[1])
+    return out
+
+
 # --------------------------------------------------------------------------
 # JSON codec (plan traces recorded from the reference front end)
 # --------------------------------------------------------------------------

@@ -19,7 +19,7 @@ from typing import Iterable
 
 from . import regions as rg
 from .initheap import poisson_tile_layout
-from .ir import KProg, TaskDesc, rect_of
+from .ir import KProg, TaskDesc, hbm_reads, rect_of
 
 
 def launch_bytes(task: TaskDesc, kp: KProg | None, temp_positions: Iterable[int], shapes, dtypes,
@@ -32,13 +32,14 @@ def launch_bytes(task: TaskDesc, kp: KProg | None, temp_positions: Iterable[int]
         wr = [a.writes for a in task.args]
     else:
         stored = {st[1] for _, _, sts in kp.nests for st in sts if st[0] == "store"}
+        loaded = hbm_reads(kp)
         rd = [False] * len(task.args)
         wr = [False] * len(task.args)
         for i, s in enumerate(kp.slots):
             if s.local:
                 continue
             a = task.args[s.arg]
-            rd[s.arg] = rd[s.arg] or a.reads
+            rd[s.arg] = rd[s.arg] or i in loaded
             wr[s.arg] = wr[s.arg] or (i in stored and a.writes)
     total = 0
     for i in sel:

@@ -1,0 +1,339 @@
+"""TEST INFRASTRUCTURE: a CPU stand-in for ``libdk_b200.so`` (multi-rank over gloo).
+
+It implements the C-ABI the executor calls, with numpy "device" memory and
+the CPU oracle as the kernel engine, so the host-side parts of the multi-GPU
+path -- point->rank mapping, the coherence planner (valid/written rects,
+transfer plans identical on every rank), partial-sum allgather and the
+point-order fold -- run for real in world-size-2 processes on CPU.  Memory
+that was never initialised or received reads as a 1e300 sentinel, so a missing
+transfer shows up as a wrong heap, not as a silent pass.
+
+Never used by the product: ``paper_2406_18109_b200`` only loads the real
+library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from oracle.interp import default_builtins, interpret
+from paper_2406_18109_b200.ir import KProg, Slot
+
+SENTINEL = 1e300
+
+
+def _set(ref, v):
+    ref._obj.value = v
+
+
+def _tokens(text):
+    return text.replace("(", " ( ").replace(")", " ) ").split()
+
+
+def parse_wire(text: str) -> KProg:
+    toks = _tokens(text)
+    pos = [0]
+
+    def nxt():
+        t = toks[pos[0]]
+        pos[0] += 1
+        return t
+
+    def offs(t):
+        return () if t == "-" else tuple(int(x) for x in t.split(","))
+
+    def expr():
+        assert nxt() == "("
+        tag = nxt()
+        if tag == "L":
+            e = ("ld", int(nxt()), offs(nxt()))
+        elif tag == "P":
+            e = ("sc", int(nxt()))
+        elif tag == "V":
+            e = ("t", int(nxt()))
+        elif tag == "C":
+            bits = int(nxt(), 16)
+            e = ("c", float(np.array([bits], dtype=np.uint64).view(np.float64)[0]))
+        elif tag == "B":
+            op = nxt()
+            e = ("bin", op, expr(), expr())
+        elif tag == "N":
+            e = ("neg", expr())
+        else:
+            e = ("sel", expr(), expr(), expr())
+        assert nxt() == ")"
+        return e
+
+    assert nxt() == "DK1"
+    nslots, nscal, ntemps, nnests = (int(nxt()) for _ in range(4))
+    slots = []
+    for i in range(nslots):
+        assert nxt() == "slot"
+        int(nxt())
+        rank = int(nxt())
+        kind = nxt()
+        priv = nxt()
+        slots.append(Slot(f"s{i}", i, kind == "L", None if priv == "-" else priv, rank))
+    nests = []
+    for _ in range(nnests):
+        assert nxt() == "nest"
+        dom, rank, ns = int(nxt()), int(nxt()), int(nxt())
+        stmts = []
+        for _ in range(ns):
+            t = nxt()
+            if t == "T":
+                stmts.append(("set", int(nxt()), expr()))
+            elif t == "S":
+                slot = int(nxt())
+                o = offs(nxt())
+                stmts.append(("store", slot, o, expr()))
+            else:
+                stmts.append(("reduce", int(nxt()), expr()))
+        nests.append((dom, rank, tuple(stmts)))
+    return KProg(tuple(slots), tuple(f"p{i}" for i in range(nscal)), ntemps, tuple(nests), True)
+
+
+class FakeLib:
+    def __init__(self, rank: int = 0, world: int = 1):
+        self.rank, self.world = rank, world
+        self.allocs: dict[int, np.ndarray] = {}  # id -> uint8 buffer
+        self.stores: dict[int, tuple] = {}  # sid -> (alloc id, shape, esize)
+        self.kernels: list[KProg] = []
+        self.next_id = 1
+        self.launches = 0
+        self.err = b""
+
+    # ---- memory helpers
+    def _alloc(self, nbytes, fill=None):
+        aid = self.next_id
+        self.next_id += 1
+        buf = np.zeros(max(nbytes, 16), dtype=np.uint8)
+        if fill is not None:
+            buf[: nbytes // 8 * 8].view(np.float64)[:] = fill
+        self.allocs[aid] = buf
+        return aid, aid << 40
+
+    def _resolve(self, ptr):
+        aid, off = ptr >> 40, ptr & ((1 << 40) - 1)
+        return self.allocs[aid], off
+
+    def _view(self, v):
+        buf, off = self._resolve(v.ptr)
+        es = 8 if v.dtype == 0 else 4
+        dt = np.float64 if v.dtype == 0 else np.int32
+        shape = tuple(v.ext[d] for d in range(v.rank))
+        strides = tuple(v.stride[d] * es for d in range(v.rank))
+        base = buf[off:].view(np.uint8)
+        return np.lib.stride_tricks.as_strided(base.view(dt) if (buf.size - off) % es == 0 else base[: (buf.size - off) // es * es].view(dt), shape=shape, strides=strides)
+
+    def _store_array(self, sid):
+        aid, shape, es = self.stores[sid]
+        dt = np.float64 if es == 8 else np.int32
+        n = int(np.prod(shape)) if shape else 1
+        return self.allocs[aid][: n * es].view(dt).reshape(shape)
+
+    # ---- ABI
+    def dk_last_error(self):
+        return self.err
+
+    def dk_init(self, device):
+        return 0
+
+    def dk_sync(self):
+        return 0
+
+    def dk_get_stream(self, ref):
+        _set(ref, 0)
+        return 0
+
+    def dk_set_stream(self, s):
+        return 0
+
+    def dk_launch_count(self, ref):
+        _set(ref, self.launches)
+        return 0
+
+    def dk_store_create(self, sid, rank, extents, dtype):
+        shape = tuple(extents[d] for d in range(rank))
+        es = 8 if dtype == 0 else 4
+        n = int(np.prod(shape)) if shape else 1
+        aid, _ = self._alloc(n * es, fill=SENTINEL if es == 8 else None)
+        self.stores[sid] = (aid, shape, es)
+        return 0
+
+    def dk_store_ptr(self, sid, ref):
+        _set(ref, self.stores[sid][0] << 40)
+        return 0
+
+    def dk_store_ensure(self, sid, lo, hi):
+        return 0
+
+    def dk_store_free(self, sid):
+        aid = self.stores.pop(sid)[0]
+        self.allocs.pop(aid, None)
+        return 0
+
+    def _rect_slices(self, sid, lo, hi):
+        shape = self.stores[sid][1]
+        return tuple(slice(lo[d], hi[d]) for d in range(len(shape)))
+
+    def _host_view(self, sid, addr):
+        aid, shape, es = self.stores[sid]
+        n = int(np.prod(shape)) if shape else 1
+        dt = ctypes.c_double if es == 8 else ctypes.c_int32
+        arr = (dt * n).from_address(addr)
+        return np.ctypeslib.as_array(arr).reshape(shape)
+
+    def dk_store_upload_rect(self, sid, lo, hi, host):
+        addr = host.value if isinstance(host, ctypes.c_void_p) else int(host)
+        sl = self._rect_slices(sid, lo, hi)
+        self._store_array(sid)[sl] = self._host_view(sid, addr)[sl]
+        return 0
+
+    def dk_store_download_rect(self, sid, lo, hi, host):
+        addr = host.value if isinstance(host, ctypes.c_void_p) else int(host)
+        sl = self._rect_slices(sid, lo, hi)
+        self._host_view(sid, addr)[sl] = self._store_array(sid)[sl]
+        return 0
+
+    def dk_store_fill(self, sid, a, b, v):
+        self._store_array(sid).reshape(-1)[a:b] = v
+        return 0
+
+    def dk_scratch_alloc(self, nbytes, ref):
+        _, ptr = self._alloc(nbytes)
+        _set(ref, ptr)
+        return 0
+
+    def dk_scratch_free(self, ptr):
+        self.allocs.pop(ptr >> 40, None)
+        return 0
+
+    def dk_memset_zero(self, ptr, nbytes):
+        buf, off = self._resolve(ptr)
+        buf[off : off + nbytes] = 0
+        return 0
+
+    def dk_kernel_compile(self, text, n, ref):
+        self.kernels.append(parse_wire(text.decode() if isinstance(text, bytes) else text))
+        _set(ref, len(self.kernels) - 1)
+        return 0
+
+    def dk_launch(self, h, views, nviews, scalars, nscal, totals):
+        kp = self.kernels[h]
+        bufs = {}
+        lshapes = {}
+        for i, s in enumerate(kp.slots):
+            v = views[i]
+            if s.local:
+                lshapes[i] = tuple(v.ext[d] for d in range(v.rank))
+            else:
+                bufs[i] = self._view(v)
+        scal = [scalars[i] for i in range(nscal)]
+        if totals:
+            # per-statement totals: retarget reduce statement k to its own zero arena
+            nests = []
+            arenas = []
+            slots = list(kp.slots)
+            for dom, rank, sts in kp.nests:
+                new = []
+                for st in sts:
+                    if st[0] == "reduce":
+                        extra = len(slots)
+                        slots.append(Slot(f"t{extra}", extra, False, "Rd", 0))
+                        bufs[extra] = np.zeros(bufs[st[1]].shape)
+                        arenas.append(bufs[extra])
+                        new.append(("reduce", extra, st[2]))
+                    else:
+                        new.append(st)
+                nests.append((dom, rank, tuple(new)))
+            kp2 = KProg(tuple(slots), kp.scalar_names, kp.ntemps, tuple(nests), kp.fused_names)
+            interpret(kp2, bufs, scal, lshapes)
+            tb, toff = self._resolve(totals)
+            out = tb[toff:].view(np.float64)
+            for k, arena in enumerate(arenas):
+                out[k] = float(arena.reshape(-1)[0])
+        else:
+            interpret(kp, bufs, scal, lshapes)
+        self.launches += 1
+        return 0
+
+    def dk_accum(self, tv, vals, first, stride, n):
+        t = self._view(tv._obj if hasattr(tv, "_obj") else tv)
+        vb, off = self._resolve(vals)
+        arr = vb[off:].view(np.float64)
+        for i in range(n):
+            t[...] += arr[first + i * stride]
+        return 0
+
+    def dk_builtin(self, kind, views, n, writes):
+        from paper_2406_18109_b200.ir import ArgDesc, NONE_PART, TaskDesc
+
+        kind = kind.decode() if isinstance(kind, bytes) else kind
+        bufs = [self._view(views[j]) for j in range(n)]
+        task = TaskDesc(kind, (1,), tuple(ArgDesc(j, NONE_PART, "W" if writes[j] else "R") for j in range(n)))
+        default_builtins()[kind](task, bufs)
+        self.launches += 1
+        return 0
+
+    # ---- collectives over torch.distributed (gloo)
+    def dk_comm_unique_id(self, buf):
+        return 0
+
+    def dk_comm_init(self, rank, world, buf):
+        return 0
+
+    def dk_comm_exchange(self, n, sids, peers, dirs, los, his):
+        import torch
+        import torch.distributed as dist
+
+        reqs = []
+        recvs = []
+        counter: dict[tuple, int] = {}
+        for i in range(n):
+            sid = sids[i]
+            shape = self.stores[sid][1]
+            r = len(shape)
+            sl = tuple(slice(los[4 * i + d], his[4 * i + d]) for d in range(r))
+            arr = self._store_array(sid)
+            peer = peers[i]
+            key = (min(self.rank, peer), max(self.rank, peer), dirs[i] if self.rank < peer else 1 - dirs[i])
+            tag = counter.get(key, 0)
+            counter[key] = tag + 1
+            if dirs[i] == 0:
+                t = torch.from_numpy(np.ascontiguousarray(arr[sl]).astype(np.float64).copy())
+                reqs.append(dist.isend(t, peer, tag=tag))
+            else:
+                t = torch.empty(arr[sl].shape, dtype=torch.float64)
+                reqs.append(dist.irecv(t, peer, tag=tag))
+                recvs.append((sid, sl, t))
+        for q in reqs:
+            q.wait()
+        for sid, sl, t in recvs:
+            self._store_array(sid)[sl] = t.numpy().astype(self._store_array(sid).dtype)
+        return 0
+
+    def dk_comm_allgather_f64(self, src, dst, count):
+        import torch
+        import torch.distributed as dist
+
+        sb, so = self._resolve(src)
+        db, do = self._resolve(dst)
+        mine = torch.from_numpy(sb[so:].view(np.float64)[:count].copy())
+        parts = [torch.empty(count, dtype=torch.float64) for _ in range(self.world)]
+        dist.all_gather(parts, mine)
+        out = db[do:].view(np.float64)
+        for q in range(self.world):
+            out[q * count : (q + 1) * count] = parts[q].numpy()
+        return 0
+
+    def dk_comm_barrier(self):
+        import torch.distributed as dist
+
+        dist.barrier()
+        return 0
+
+    def dk_comm_destroy(self):
+        return 0

@@ -1,0 +1,72 @@
+"""torchrun worker: golden multi-point plans on N real GPUs (NCCL), compared on rank 0.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_worker.py
+"""
+
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from conftest import golden_arrays, load_golden, same_bits  # noqa: E402
+from paper_2406_18109_b200.executor import Executor, replay  # noqa: E402
+from paper_2406_18109_b200.plan import PlanTrace  # noqa: E402
+
+NAMES = [
+    "stencil/fused", "stencil/unfused", "blackscholes_chain/fused", "blackscholes_chain/unfused",
+    "jacobi/fused", "cg_like/fused", "cg_like/unfused",
+    "stencil_bands_n8_k2/fused", "stencil_bands_n8_k2/unfused", "stencil_bands_n6_k4/fused",
+    "cg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused", "cg_csr_6x12_k4/unfused", "pcg_csr_8x8_k2/fused",
+]
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    cases = {c["name"]: c for c in load_golden("bench_small.json.gz") + load_golden("fuzz250.json.gz")}
+    names = NAMES + [f"fuzz{s}/fused" for s in range(0, 250, 5)]
+    bad, moved, exact, close = [], 0, 0, 0
+    uid = None
+    for name in names:
+        case = cases[name]
+        tr = PlanTrace.from_json(case["trace"])
+        ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes, rank=rank, world=world,
+                      device=local)
+        if uid is None:
+            obj = [ex.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ex.init_comm(obj[0])
+            uid = True
+        else:
+            ex._comm = True
+        replay(ex, tr.events)
+        got = {s: ex.get(s) for s in tr.live}
+        moved += ex.stats.transfers
+        ex.close()
+        if rank == 0:
+            for s, w in golden_arrays(case).items():
+                if same_bits(got[s], w):
+                    exact += 1
+                elif np.allclose(got[s], w, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(w))))):
+                    close += 1
+                else:
+                    bad.append((name, s))
+    if rank == 0:
+        print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved}")
+        if bad:
+            sys.exit(1)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

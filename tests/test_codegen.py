@@ -81,12 +81,17 @@ def test_fused_blackscholes_kernel_is_one_register_nest(rt):
     case = {c["name"]: c for c in load_golden("bench_small.json.gz")}["blackscholes_chain/fused"]
     tr = PlanTrace.from_json(case["trace"])
     big = [e for e in tr.execs() if e.f == 67][0]
-    src = codegen(rt, big.kernel, views_for(rt, big.task, big.kernel, tr.shapes), compile_=False)
-    assert src.count("__global__") == 1
-    # 66 SetTemps per lane live in registers; only x, y are loaded and out stored
-    assert src.count("dk_ldp(") == 2 + 1  # two loads + the helper definition
-    assert src.count("dk_stp(") == 1 + 1
-    assert "dk_mul(" in src and "dk_neg(" in src
+    src = codegen(rt, big.kernel, views_for(rt, big.task, big.kernel, tr.shapes), compile_=False,
+                  scalars=big.task.scalars)
+    body = src[src.index("__global__"):]
+    assert body.count("__global__") == 1
+    # 66 SetTemps per lane live in registers; only x, y are loaded and out stored,
+    # as 16-byte aligned pairs
+    assert body.count("dk_ld_A(") == 2 and body.count("dk_st_A(") == 1
+    assert "dk_ld_C(" not in body and "dk_st_C(" not in body
+    assert "dk_mul(" in body and "dk_neg(" in body
+    # 26 task scalars, two distinct values: only two parameter slots are read
+    assert sorted(set(body.split("P.sc[")[i].split("]")[0] for i in range(1, body.count("P.sc[") + 1))) == ["0", "1"]
 
 
 def test_privilege_violation_detected_without_device(rt):
