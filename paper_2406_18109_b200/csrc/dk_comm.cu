@@ -83,7 +83,11 @@ int dk_comm_unique_id(uint8_t* out128) {
 int dk_comm_init(int rank, int world, const uint8_t* id128) {
   return guard([&] {
     require_init();
-    if (st().comm) fail(DK_ERR_STATE, "communicator already initialised");
+    if (st().comm) {
+      // one communicator per process; later executors of the same job reuse it
+      if (st().rank == rank && st().world == world) return;
+      fail(DK_ERR_STATE, "communicator already initialised for rank %d of %d", st().rank, st().world);
+    }
     ncclUniqueId id;
     memcpy(&id, id128, 128);
     ncclComm_t c;

@@ -418,6 +418,8 @@ class Executor:
                 if rg.empty(rect):
                     continue
                 if reads[j]:
+                    if kp is None and task.kind == "SPMV_CSR" and j == 3:
+                        rect = self._csr_footprint(task, pts[i], rect)
                     need.setdefault(q, {}).setdefault(a.store, []).append(rect)
                 if reduces[j]:
                     if multi and a.part.is_none:
@@ -453,6 +455,24 @@ class Executor:
                     for o in range(self.world):
                         r.valid[o] = rg.add(r.valid[o], r.full)
                     r.written = rg.add(r.written, r.full)
+
+    def _csr_footprint(self, task: TaskDesc, p, full):
+        """Columns of x an SPMV_CSR tile actually reads (NonePart reads the whole store).
+
+        For the Poisson tiles (init spec known on every rank) the referenced
+        columns are the tile's rows +- one grid row; the coherence planner
+        then moves a one-row halo instead of gathering all of x.  Unknown
+        matrices keep the conservative whole-store footprint.
+        """
+        spec = self.init.get(task.args[1].store)
+        if not spec or spec.get("kind") != "csr_cols":
+            return full
+        lay = poisson_tile_layout(int(spec["nx"]), int(spec["ny"]), int(spec["k"]))
+        t, nx, n = lay["t"], lay["nx"], lay["n"]
+        q = p[0]
+        if full[1][0] != n:
+            return full
+        return ((max(0, q * t - nx),), (min(n, (q + 1) * t + nx),))
 
     def _access(self, kp: KProg):
         hit = self._acc.get(id(kp))
