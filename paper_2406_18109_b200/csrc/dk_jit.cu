@@ -230,10 +230,27 @@ struct Site {
   int slot;
   std::vector<int64_t> offs;  // empty = zero offsets
   char cls;                   // S scalar, C contiguous inner, B broadcast inner, G strided inner
+  bool staged = false;        // read through the CTA's TMA-staged tile (K3)
+  int dr = 0, dc = 0;         // element offset of this view within the staged tile
 };
+
+// K3: aliased views of one store (the stencil's shifted interior views) are
+// staged tile by tile in shared memory by TMA and read from there; each
+// CTA owns a persistent loop over TR x TC output tiles with a 2-stage
+// mbarrier pipeline.
+static const int kTR = 8;     // output rows per tile
+static const int kTC = 128;   // output columns per tile (64 element pairs)
+static const int kBW = 136;   // TMA box width (tile + column halo + alignment), 1088 B per row
 
 struct NestPlan {
   int rank = 0;  // actual domain rank
+  bool staged = false;
+  int st_rows = 0;         // box rows = kTR + max dr
+  int st_sh = 0;           // column shift that 16-byte aligns the tensor base
+  int st_anchor = -1;      // site whose view origin is the group's minimum address
+  int st_min_dc = 0;
+  uint64_t st_base = 0;    // tensor base address (aligned)
+  int64_t st_cols = 0, st_nrows = 0, st_rowstride = 0;
   std::vector<Site> sites;
   std::vector<char> site_loaded;   // site read before any store to its slot (phase-1 load)
   std::vector<int> red_slots;      // target slot per reduce statement (statement order)
@@ -273,9 +290,73 @@ static bool bcast_strides(const dk_view& v, const int64_t* D, int r, int64_t* ou
   return true;
 }
 
+// Decide whether a rank-2 nest reads >= 3 views of one store at small constant
+// offsets (read-only in the whole kernel): those views are served from one TMA
+// tile per CTA instead of 3-5 overlapping global streams.
+static void plan_staging(NestPlan& np, const dk_view* views, const int64_t* D, int r, const std::set<int>& kstored) {
+  if (r != 2 || D[0] < kTR || D[1] < 64 || getenv("DK_JIT_NO_K3")) return;
+  std::vector<int> cand;
+  for (size_t i = 0; i < np.sites.size(); ++i) {
+    const Site& s = np.sites[i];
+    if (!np.site_loaded[i] || !s.offs.empty() || (s.cls != 'A' && s.cls != 'C') || kstored.count(s.slot)) continue;
+    const dk_view& v = views[s.slot];
+    if (v.rank != 2 || v.ext[0] != D[0] || v.ext[1] != D[1] || v.stride[1] != 1) continue;
+    cand.push_back((int)i);
+  }
+  // group by row stride; take the largest group
+  std::map<int64_t, std::vector<int>> by;
+  for (int i : cand) by[views[np.sites[i].slot].stride[0]].push_back(i);
+  std::vector<int> best;
+  int64_t rs = 0;
+  for (auto& kv : by)
+    if (kv.second.size() > best.size()) best = kv.second, rs = kv.first;
+  if (best.size() < 3 || (rs * 8) % 16 != 0 || rs <= 16) return;
+  uint64_t anchor = ~0ull;
+  int anchor_i = -1;
+  for (int i : best)
+    if (views[np.sites[i].slot].ptr < anchor) anchor = views[np.sites[i].slot].ptr, anchor_i = i;
+  std::vector<int> grp;
+  int min_dc = 0, max_dc = 0, max_dr = 0;
+  for (int i : best) {
+    int64_t d = (int64_t)(views[np.sites[i].slot].ptr - anchor);
+    if (d % 8) continue;
+    d /= 8;
+    int64_t dr = (d + 8) / rs, dc = d - dr * rs;
+    if (dr > 4 || dc < -8 || dc > 8) continue;
+    np.sites[i].dr = (int)dr;
+    np.sites[i].dc = (int)dc;
+    grp.push_back(i);
+  }
+  if (grp.size() < 3) return;
+  for (int i : grp) {
+    min_dc = std::min(min_dc, np.sites[i].dc);
+    max_dc = std::max(max_dc, np.sites[i].dc);
+    max_dr = std::max(max_dr, np.sites[i].dr);
+  }
+  uint64_t base = anchor + 8ull * (uint64_t)(int64_t)min_dc;  // min_dc <= 0
+  int sh = (int)((base % 16) / 8);
+  base -= 8ull * sh;
+  if (max_dc - min_dc + sh + kTC > kBW) return;
+  if (D[1] + (max_dc - min_dc) + sh > rs) return;  // the union must not wrap across rows
+  np.staged = true;
+  np.st_rows = kTR + max_dr;
+  np.st_sh = sh;
+  np.st_anchor = anchor_i;
+  np.st_min_dc = min_dc;
+  np.st_base = base;
+  np.st_cols = D[1] + (max_dc - min_dc) + sh;
+  np.st_nrows = D[0] + max_dr;
+  np.st_rowstride = rs;
+  for (int i : grp) np.sites[i].staged = true;
+}
+
 static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std::string* key) {
   std::vector<NestPlan> plans;
   std::ostringstream ks;
+  std::set<int> kstored;  // slots stored anywhere in the kernel
+  for (const NestIR& ne : g.nests)
+    for (const Stmt& s : ne.stmts)
+      if (s.tag == 'S') kstored.insert(s.target);
   for (size_t n = 0; n < g.nests.size(); ++n) {
     const NestIR& ne = g.nests[n];
     const dk_view& dv = views[ne.dom];
@@ -381,8 +462,11 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
     for (const Site& s : np.sites) {
       if (r == 0 && s.cls != 'S') fail(DK_ERR_UNSUPPORTED, "rank-0 nest over an array operand");
     }
+    plan_staging(np, views, D, r, kstored);
     ks << "n" << n << ":r" << r << ":";
+    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << ";";
     for (const Site& s : np.sites) {
+      if (s.staged) ks << "s" << s.dr << "," << s.dc;
       ks << s.slot << s.cls;
       for (auto o : s.offs) ks << "," << o;
       ks << ";";
@@ -453,6 +537,30 @@ __device__ __forceinline__ void dk_st_C(double* p, int64_t e, bool full, double 
 }
 __device__ __forceinline__ void dk_st_G(double* p, int64_t e, bool full, double x, double y, int64_t s) {
   p[e * s] = x; if (full) p[(e + 1) * s] = y;
+}
+
+// ---- K3: TMA tile staging (cp.async.bulk.tensor + mbarrier) ----
+__device__ __forceinline__ uint32_t dk_smem(const void* p) {
+  uint64_t a;
+  asm("cvta.to.shared.u64 %0, %1;" : "=l"(a) : "l"(p));
+  return (uint32_t)a;
+}
+__device__ __forceinline__ void dk_mbar_init(uint32_t bar, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void dk_fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void dk_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void dk_tma_2d(const void* tmap, uint32_t bar, uint32_t dst, int c0, int c1, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void dk_mbar_wait(uint32_t bar, uint32_t ph) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(bar), "r"(ph) : "memory");
 }
 
 __device__ __forceinline__ double dk_warp_sum(double v) {
@@ -581,16 +689,97 @@ class Gen {
     fail(DK_ERR_ARG, "bad expression");
   }
 
+  // K3: persistent CTAs walk kTR x kTC output tiles; thread 0 keeps the next
+  // tile's TMA load in flight (2 stages, one mbarrier each) while all 256
+  // threads compute the current one from shared memory.  Thread t owns the
+  // element pair (t & 63) of rows (t >> 6) and (t >> 6) + 4 of the tile.
+  void nest_staged(std::ostringstream& o, int n, const std::vector<int>& wslots) const {
+    const NestIR& ne = g_.nests[n];
+    const NestPlan& np = plans_[n];
+    const int NS = (int)np.sites.size();
+    const int NR = (int)np.red_slots.size();
+    const int ROWS = np.st_rows;
+    const unsigned bytes = (unsigned)(ROWS * kBW * 8);
+    for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
+    // even row count per stage keeps stage 1 on a 128-byte boundary (TMA destination alignment)
+    o << "  __shared__ __align__(128) double dk_tile[2][" << (ROWS + 1) / 2 * 2 << "][" << kBW << "];\n";
+    o << "  __shared__ __align__(8) unsigned long long dk_bar[2];\n";
+    o << "  const int tid = threadIdx.x;\n";
+    o << "  const int64_t D0 = P.h.ext[0], D1 = P.h.ext[1];\n";
+    o << "  const int64_t ntc = (D1 + " << kTC - 1 << ") / " << kTC << ", ntiles = ((D0 + " << kTR - 1 << ") / " << kTR
+      << ") * ntc;\n";
+    o << "  const uint32_t bar0 = dk_smem(&dk_bar[0]), bar1 = dk_smem(&dk_bar[1]);\n";
+    o << "  if (tid == 0) { dk_mbar_init(bar0, 1); dk_mbar_init(bar1, 1); dk_fence_mbar_init(); }\n";
+    o << "  __syncthreads();\n";
+    o << "  int64_t tile = blockIdx.x;\n";
+    o << "  if (tid == 0 && tile < ntiles)\n    dk_tma_2d(&P.tm, bar0, dk_smem(&dk_tile[0][0][0]), (int)((tile % ntc) * " << kTC
+      << "), (int)((tile / ntc) * " << kTR << "), " << bytes << "u);\n";
+    o << "  const int pr = tid & 63, rg = tid >> 6;\n";
+    o << "  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {\n";
+    o << "    const int stg = it & 1;\n    const uint32_t ph = (uint32_t)((it >> 1) & 1);\n";
+    o << "    const int64_t nxt = tile + gridDim.x;\n";
+    o << "    if (tid == 0 && nxt < ntiles) {\n      dk_fence_proxy_async();\n";
+    o << "      dk_tma_2d(&P.tm, stg ? bar0 : bar1, dk_smem(&dk_tile[stg ^ 1][0][0]), (int)((nxt % ntc) * " << kTC
+      << "), (int)((nxt / ntc) * " << kTR << "), " << bytes << "u);\n    }\n";
+    o << "    dk_mbar_wait(stg ? bar1 : bar0, ph);\n";
+    o << "    const int64_t r0 = (tile / ntc) * " << kTR << ", c0 = (tile % ntc) * " << kTC << ";\n";
+    o << "    const double (*T)[" << kBW << "] = dk_tile[stg];\n";
+    for (int i = 0; i < NS; ++i)
+      if (np.sites[i].cls != 'S' && np.site_loaded[i]) o << "    double2 v" << i << "[2];\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < 2; ++u) {\n";
+    o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
+    o << "      if (row < D0 && e < D1) {\n        const bool full = e + 1 < D1;\n";
+    for (int i = 0; i < NS; ++i) {
+      const Site& s = np.sites[i];
+      if (s.cls == 'S' || !np.site_loaded[i]) continue;
+      if (s.staged) {
+        const int col = s.dc - np.st_min_dc + np.st_sh;  // tile column of element pair 0
+        o << "        { const double* t = &T[a + " << s.dr << "][2 * pr + " << col << "]; ";
+        if (col % 2 == 0)
+          o << "v" << i << "[u] = full ? *reinterpret_cast<const double2*>(t) : make_double2(t[0], 0.0); }\n";
+        else
+          o << "v" << i << "[u].x = t[0]; v" << i << "[u].y = full ? t[1] : 0.0; }\n";
+      } else {
+        const char c = s.cls;
+        o << "        v" << i << "[u] = dk_ld_" << c << "((double*)P.s[" << i << "].p + row * P.s[" << i
+          << "].st[0], e, full";
+        if (c == 'G') o << ", P.s[" << i << "].sti";
+        o << ");\n";
+      }
+    }
+    o << "      }\n    }\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < 2; ++u) {\n";
+    o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
+    o << "      if (row < D0 && e < D1) {\n        const bool full = e + 1 < D1;\n";
+    for (int w : wslots) o << "        double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
+    o << "        {\n" << lane_code(np, ne, "x") << "        }\n";
+    o << "        if (full) {\n" << lane_code(np, ne, "y") << "        }\n";
+    for (int w : wslots) {
+      int si = site_index(np, w, {});
+      const char c = np.sites[si].cls;
+      o << "        dk_st_" << c << "((double*)P.s[" << si << "].p + row * P.s[" << si << "].st[0], e, full, w" << w
+        << "_x, w" << w << "_y";
+      if (c == 'G') o << ", P.s[" << si << "].sti";
+      o << ");\n";
+    }
+    o << "      }\n    }\n";
+    o << "    __syncthreads();\n  }\n";
+    if (NR) emit_reduce_epilogue(o, np, ne, wslots);
+    o << "}\n";
+  }
+
   void nest(std::ostringstream& o, int n) const {
     const NestIR& ne = g_.nests[n];
     const NestPlan& np = plans_[n];
     const int r = np.rank;
     const int NS = (int)np.sites.size();
     const int NR = (int)np.red_slots.size();
-    o << "\nstruct P" << n << " { DkHdr h; DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
+    o << "\nstruct P" << n << " { ";
+    if (np.staged) o << "alignas(64) unsigned char tm[128]; ";
+    o << "DkHdr h; DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_ << "_n" << n
-      << "(const P" << n << " P) {\n";
+      << "(const __grid_constant__ P" << n << " P) {\n";
     // hoisted rank-0 operands
     for (int i = 0; i < NS; ++i)
       if (np.sites[i].cls == 'S') o << "  const double S" << i << " = *(const double*)P.s[" << i << "].p;\n";
@@ -606,6 +795,10 @@ class Gen {
       for (int w : wslots) o << "  double w" << w << "_s = 0.0;\n";
       emit_scalar_seq(o, np, ne, /*apply_reduce=*/true, wslots);
       o << "}\n";
+      return;
+    }
+    if (np.staged) {
+      nest_staged(o, n, wslots);
       return;
     }
 
@@ -879,9 +1072,10 @@ struct KernelObj {
 
 static std::vector<std::unique_ptr<KernelObj>> g_kernels;
 
-static Module* get_module(KernelObj& k, const dk_view* views, const double* scalars) {
+static Module* get_module(KernelObj& k, const dk_view* views, const double* scalars, std::vector<NestPlan>* fresh) {
   std::string key;
   std::vector<NestPlan> plans = plan_nests(k.prog, views, &key);
+  *fresh = plans;  // pointer-dependent fields (TMA tensor base) come from this binding
   // bitwise-equal scalar classes are part of the binding class
   std::vector<int> rep(k.prog.nscal);
   for (int i = 0; i < k.prog.nscal; ++i) {
@@ -958,12 +1152,13 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   const Prog& g = k.prog;
   if (nviews != g.nslots) fail(DK_ERR_ARG, "launch binds %d views, kernel has %d slots", nviews, g.nslots);
   if (nscal != g.nscal) fail(DK_ERR_ARG, "launch passes %d scalars, kernel expects %d", nscal, g.nscal);
-  Module* m = get_module(k, views, scalars);
+  std::vector<NestPlan> fresh;
+  Module* m = get_module(k, views, scalars, &fresh);
   State& S = st();
   int kbase = 0;
   std::vector<char> blob;
   for (size_t n = 0; n < g.nests.size(); ++n) {
-    const NestPlan& np = m->plans[n];
+    const NestPlan& np = fresh[n];
     const dk_view& dv = views[g.nests[n].dom];
     const int r = np.rank;
     DkHdr h = {};
@@ -1001,8 +1196,24 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     memset(rd.data(), 0, sizeof(dk_view) * rd.size());
     for (int q = 0; q < NR; ++q) rd[q] = views[np.red_slots[q]];
     const size_t nsc = std::max(g.nscal, 1);
-    blob.assign(sizeof(DkHdr) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc, 0);
+    const size_t tmb = np.staged ? 128 : 0;  // CUtensorMap (64-byte aligned) leads a staged nest's params
+    size_t total = tmb + sizeof(DkHdr) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc;
+    if (np.staged) total = (total + 63) / 64 * 64;
+    blob.assign(total + 64, 0);
     char* p = blob.data();
+    if (np.staged) {
+      static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+      CUtensorMap tm;
+      cuuint64_t gdim[2] = {(cuuint64_t)np.st_cols, (cuuint64_t)np.st_nrows};
+      cuuint64_t gstr[1] = {(cuuint64_t)np.st_rowstride * 8};
+      cuuint32_t box[2] = {(cuuint32_t)kBW, (cuuint32_t)np.st_rows};
+      cuuint32_t estr[2] = {1, 1};
+      DK_CU(cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)np.st_base, gdim, gstr, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+      memcpy(p, &tm, 128);
+      p += 128;
+    }
     memcpy(p, &h, sizeof h);
     p += sizeof h;
     memcpy(p, sites.data(), sizeof(DkSite) * sites.size());
@@ -1028,10 +1239,16 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       tx = 32;
       ty = 1;
     }
-    size_t bsz = blob.size();
-    void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, blob.data(), CU_LAUNCH_PARAM_BUFFER_SIZE, &bsz,
-                     CU_LAUNCH_PARAM_END};
-    DK_CU(cuLaunchKernel(m->fn[n], gx, gy, 1, tx, ty, 1, 0, (CUstream)S.stream, nullptr, extra));
+    if (np.staged) {
+      const int64_t ntiles = ((D[0] + kTR - 1) / kTR) * ((D[1] + kTC - 1) / kTC);
+      gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)S.sm_count * m->occ[n]));
+      gy = 1;
+      tx = kTPB;
+      ty = 1;
+    }
+    // one by-value struct parameter; the driver copies sizeof(P_n) bytes from the blob
+    void* args[] = {blob.data()};
+    DK_CU(cuLaunchKernel(m->fn[n], gx, gy, 1, tx, ty, 1, 0, (CUstream)S.stream, args, nullptr));
     S.launches++;
     kbase += NR;
   }

@@ -644,7 +644,9 @@ class Executor:
         """Replace the whole store with ``host`` (every rank holds it valid)."""
         r = self.rec(sid)
         np_dtype = np.float64 if r.dtype == "f64" else np.int32
-        a = np.ascontiguousarray(host, dtype=np_dtype)
+        a = np.asarray(host, dtype=np_dtype)  # (ascontiguousarray would turn 0-d into (1,))
+        if not a.flags.c_contiguous:
+            a = a.copy(order="C")
         if a.shape != r.shape:
             raise ValueError(f"store {sid} has shape {r.shape}, got {a.shape}")
         self._ensure(r, r.full)

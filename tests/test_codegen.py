@@ -36,7 +36,7 @@ def views_for(rt, task, kp, shapes, point=None):
         for d in range(len(shape) - 2, -1, -1):
             strides[d] = strides[d + 1] * shape[d + 1]
         v = views[i]
-        v.ptr = base * (i + 1) + 8 * sum(l * st for l, st in zip(lo, strides))
+        v.ptr = base * (a.store + 1) + 8 * sum(l * st for l, st in zip(lo, strides))  # one base per store
         v.rank = len(shape)
         v.dtype = 0
         for d in range(len(shape)):
