@@ -78,6 +78,18 @@ int dk_store_upload_rect(int64_t sid, const int64_t* lo, const int64_t* hi, cons
 int dk_store_download_rect(int64_t sid, const int64_t* lo, const int64_t* hi, void* host);
 int dk_store_fill(int64_t sid, int64_t elem_lo, int64_t elem_hi, double value);
 
+/* Initial contents on the device, bit-identical to numpy's PCG64 streams
+ * (Heap.get, executor.py:57-60).  state/inc = {hi, lo} of
+ * default_rng(...).bit_generator.state.  dk_pcg64_rejects lists (sorted) the
+ * draw indices < draw_end that integers(1, 10) rejects; dk_pcg64_fill writes
+ * the rect [lo, hi) of a rank-1/2 f64 store: kind 0 = integers(1, 10) with
+ * rejection breakpoints `breaks` (element index after which the draw index
+ * shifts by one more), kind 1 = random() * scale. */
+int dk_pcg64_rejects(const uint64_t* state, const uint64_t* inc, int64_t draw_end, int64_t* out, int64_t cap,
+                     int64_t* count);
+int dk_pcg64_fill(int64_t sid, const int64_t* lo, const int64_t* hi, const uint64_t* state, const uint64_t* inc,
+                  int kind, double scale, const int64_t* breaks, int64_t nbreaks);
+
 /* scratch (task-local buffers, staging): stream-ordered */
 int dk_scratch_alloc(int64_t bytes, uint64_t* dptr);
 int dk_scratch_free(uint64_t dptr);

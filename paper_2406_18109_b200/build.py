@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdk_b200.so")
-SOURCES = ["dk_runtime.cu", "dk_kernels.cu", "dk_jit.cu", "dk_comm.cu"]
+SOURCES = ["dk_runtime.cu", "dk_kernels.cu", "dk_jit.cu", "dk_comm.cu", "dk_pcg.cu"]
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 
 

@@ -28,6 +28,7 @@ replicated target is bit-identical on all ranks.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import byref, c_double, c_int, c_int32, c_int64, c_uint8, c_uint64
 from dataclasses import dataclass, field
 from typing import Iterable, Mapping, Sequence
@@ -42,6 +43,7 @@ from .ir import KProg, TaskDesc, rect_of, slot_access
 from .runtime import DK_F64, DK_I32, check, dk_view, i64s
 
 BUILTIN_KINDS = ("MATVEC", "SPMV", "NORM", "OPAQUE", "SPMV_CSR")
+DEVICE_INIT_MIN = 1 << 16  # stores at least this large get their initial contents from dk_pcg64_fill
 
 
 @dataclass
@@ -54,6 +56,7 @@ class StoreRec:
     on_device: bool = False
     base: int = 0
     strides: tuple[int, ...] = ()
+    pcg: tuple | None = None  # (elements covered, rejection breakpoints) of the default init stream
 
     @property
     def esize(self) -> int:
@@ -192,6 +195,10 @@ class Executor:
         if kind in ("csr_rowptr", "csr_cols", "csr_vals"):
             self._materialize_csr(r, spec, rects, np_dtype)
             return
+        if (kind is None or kind == "uniform") and r.dtype == "f64" and len(r.shape) in (1, 2) \
+                and int(np.prod(r.shape)) >= DEVICE_INIT_MIN and not os.environ.get("DK_HOST_INIT"):
+            self._materialize_pcg(r, spec, rects)
+            return
         if not r.shape:
             host = host_contents(spec, self.seed, r.sid, r.shape).astype(np_dtype)
             check(self.lib.dk_store_upload_rect(r.sid, i64s([0]), i64s([0]), host.ctypes.data))
@@ -211,6 +218,39 @@ class Executor:
                 hi = (hi0,) + x[1][1:]
                 check(self.lib.dk_store_upload_rect(r.sid, i64s(lo), i64s(hi), ctypes.c_void_p(base)))
             check(self.lib.dk_sync())  # the chunk buffer is reused by the generator
+
+    def _materialize_pcg(self, r: StoreRec, spec: dict | None, rects: list) -> None:
+        """Device-side PCG64: same bits as numpy's stream, only this rank's rects (csrc/dk_pcg.cu)."""
+        if spec is None:
+            key, kind, scale = [self.seed, r.sid], 0, 1.0
+        else:
+            key, kind = [int(spec.get("seed", 0)), int(spec.get("key", r.sid))], 1
+            scale = float(spec["scale"]) if "scale" in spec else 1.0
+        s = np.random.default_rng(key).bit_generator.state["state"]
+        m64 = (1 << 64) - 1
+        st = (c_uint64 * 2)(s["state"] >> 64, s["state"] & m64)
+        inc = (c_uint64 * 2)(s["inc"] >> 64, s["inc"] & m64)
+        breaks: list[int] = []
+        if kind == 0:
+            emax = max(rg.bbox_flat(r.shape, x)[1] for x in rects)
+            if r.pcg is None or r.pcg[0] < emax:
+                d_end = emax + 64
+                while True:
+                    cap = 1 << 16
+                    out = (c_int64 * cap)()
+                    cnt = c_int64()
+                    check(self.lib.dk_pcg64_rejects(st, inc, d_end, out, cap, byref(cnt)))
+                    if cnt.value > cap:
+                        raise BackendError("PCG64 stream has more rejections than expected")
+                    if emax + cnt.value <= d_end:
+                        break
+                    d_end = emax + cnt.value + 64
+                qs = list(out[: cnt.value])
+                r.pcg = (emax, [q - k for k, q in enumerate(qs)])
+            breaks = r.pcg[1]
+        barr = (c_int64 * max(len(breaks), 1))(*breaks)
+        for x in rects:
+            check(self.lib.dk_pcg64_fill(r.sid, i64s(x[0]), i64s(x[1]), st, inc, kind, scale, barr, len(breaks)))
 
     def _materialize_csr(self, r: StoreRec, spec: dict, rects: list, np_dtype) -> None:
         nx, ny, k = int(spec["nx"]), int(spec["ny"]), int(spec["k"])

@@ -56,6 +56,15 @@ _SIGS = {
     "dk_store_upload_rect": (c_int, [c_int64, POINTER(c_int64), POINTER(c_int64), c_void_p]),
     "dk_store_download_rect": (c_int, [c_int64, POINTER(c_int64), POINTER(c_int64), c_void_p]),
     "dk_store_fill": (c_int, [c_int64, c_int64, c_int64, c_double]),
+    "dk_pcg64_rejects": (
+        c_int,
+        [POINTER(c_uint64), POINTER(c_uint64), c_int64, POINTER(c_int64), c_int64, POINTER(c_int64)],
+    ),
+    "dk_pcg64_fill": (
+        c_int,
+        [c_int64, POINTER(c_int64), POINTER(c_int64), POINTER(c_uint64), POINTER(c_uint64), c_int, c_double,
+         POINTER(c_int64), c_int64],
+    ),
     "dk_scratch_alloc": (c_int, [c_int64, POINTER(c_uint64)]),
     "dk_scratch_free": (c_int, [c_uint64]),
     "dk_memset_zero": (c_int, [c_uint64, c_int64]),

@@ -164,3 +164,68 @@ def test_nan_signed_zero_min_max_semantics(Executor):
         assert np.array_equal(np.signbit(got), np.signbit(np.negative(a)))
     finally:
         ex.close()
+
+
+def test_device_pcg64_init_matches_numpy(Executor):
+    """dk_pcg64_fill reproduces default_rng([seed, sid]).integers(1, 10) / .random() bit for bit."""
+    from paper_2406_18109_b200.initheap import host_contents
+
+    cases = [
+        ((300_001,), None, [((0,), (300_001,))]),
+        ((700, 513), None, [((0, 0), (700, 513)), ((3, 1), (650, 512)), ((0, 0), (1, 513)), ((699, 0), (700, 513))]),
+        ((1000, 300), None, [((0, 0), (1000, 1)), ((0, 299), (1000, 300)), ((17, 5), (18, 250))]),
+        ((250_000,), {"kind": "uniform", "seed": 0, "key": 1000}, [((5,), (249_990,))]),
+        ((250_000,), {"kind": "uniform", "seed": 0, "key": 1000, "scale": 0.25}, [((0,), (250_000,))]),
+    ]
+    for seed in (0, 3):
+        for sid, (shape, spec, rects) in enumerate(cases):
+            ex = Executor(shapes={sid: shape}, seed=seed, init={sid: spec} if spec else {}, device=0)
+            try:
+                r = ex.rec(sid)
+                ex._materialize_init(r, rects)
+                for o in range(ex.world):
+                    r.valid[o] = list(rects)
+                want = host_contents(spec, seed, sid, shape)
+                got = np.full(shape, np.nan)
+                for rect in rects:
+                    ex.download_local(sid, got, rect)
+                    sl = tuple(slice(l, h) for l, h in zip(*rect))
+                    assert np.array_equal(got[sl], want[sl]), (seed, sid, rect)
+            finally:
+                ex.close()
+
+
+def test_device_pcg64_rejection_path(Executor):
+    """A stream with an early Lemire rejection: the element->draw shift must match numpy."""
+    import ctypes
+
+    from paper_2406_18109_b200.runtime import check
+
+    ex = Executor(shapes={}, device=0)
+    try:
+        found = None
+        for sid in range(4000):
+            s = np.random.default_rng([0, sid]).bit_generator.state["state"]
+            m64 = (1 << 64) - 1
+            st = (ctypes.c_uint64 * 2)(s["state"] >> 64, s["state"] & m64)
+            inc = (ctypes.c_uint64 * 2)(s["inc"] >> 64, s["inc"] & m64)
+            out = (ctypes.c_int64 * 64)()
+            n = ctypes.c_int64()
+            check(ex.lib.dk_pcg64_rejects(st, inc, 3_000_000, out, 64, ctypes.byref(n)))
+            if n.value:
+                found = (sid, out[0])
+                break
+        assert found is not None, "no early rejection found"
+        sid, q = found
+        n = int(q) + 5000
+        ex.shapes[sid] = (n,)
+        r = ex.rec(sid)
+        ex._materialize_init(r, [((0,), (n,))])
+        r.valid[0] = [((0,), (n,))]
+        got = np.empty(n)
+        ex.download_local(sid, got, ((0,), (n,)))
+        want = np.random.default_rng([0, sid]).integers(1, 10, size=n).astype(np.float64)
+        assert np.array_equal(got, want)
+        assert r.pcg is not None and len(r.pcg[1]) >= 1
+    finally:
+        ex.close()
