@@ -98,6 +98,16 @@ int dk_memcpy_d2h(void* host, uint64_t dptr, int64_t bytes);   /* synchronising 
 int dk_memcpy_h2d(uint64_t dptr, const void* host, int64_t bytes);
 int dk_host_alloc(int64_t bytes, void** host);                  /* pinned */
 int dk_host_free(void* host);
+int dk_memcpy_d2h_async(void* host, uint64_t dptr, int64_t bytes);
+
+/* extra streams / events for host-streamed execution (copy-compute overlap);
+ * every enqueueing call uses the current stream (dk_set_stream) */
+int dk_stream_new(uint64_t* stream);
+int dk_event_new(uint64_t* event);
+int dk_event_record(uint64_t event);       /* on the current stream */
+int dk_stream_wait_event(uint64_t event);  /* current stream waits */
+int dk_event_sync(uint64_t event);
+int dk_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 
 /* JIT: program text (paper_2406_18109_b200.ir.KProg.wire) -> handle.
  * Compilation to sm_100a happens at first launch per binding class. */

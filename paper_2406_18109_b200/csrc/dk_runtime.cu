@@ -443,6 +443,47 @@ int dk_memcpy_h2d(uint64_t dptr, const void* host, int64_t bytes) {
   });
 }
 
+int dk_memcpy_d2h_async(void* host, uint64_t dptr, int64_t bytes) {
+  return guard([&] {
+    require_init();
+    DK_CUDA(cudaMemcpyAsync(host, (void*)dptr, bytes, cudaMemcpyDeviceToHost, st().stream));
+  });
+}
+
+int dk_stream_new(uint64_t* stream) {
+  return guard([&] {
+    require_init();
+    cudaStream_t s;
+    DK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = (uint64_t)s;
+  });
+}
+
+int dk_event_new(uint64_t* event) {
+  return guard([&] {
+    require_init();
+    cudaEvent_t e;
+    DK_CUDA(cudaEventCreate(&e));
+    *event = (uint64_t)e;
+  });
+}
+
+int dk_event_record(uint64_t event) {
+  return guard([&] { DK_CUDA(cudaEventRecord((cudaEvent_t)event, st().stream)); });
+}
+
+int dk_stream_wait_event(uint64_t event) {
+  return guard([&] { DK_CUDA(cudaStreamWaitEvent(st().stream, (cudaEvent_t)event, 0)); });
+}
+
+int dk_event_sync(uint64_t event) {
+  return guard([&] { DK_CUDA(cudaEventSynchronize((cudaEvent_t)event)); });
+}
+
+int dk_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms) {
+  return guard([&] { DK_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop)); });
+}
+
 int dk_host_alloc(int64_t bytes, void** host) {
   return guard([&] {
     require_init();

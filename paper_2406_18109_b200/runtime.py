@@ -72,6 +72,13 @@ _SIGS = {
     "dk_memcpy_h2d": (c_int, [c_uint64, c_void_p, c_int64]),
     "dk_host_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
     "dk_host_free": (c_int, [c_void_p]),
+    "dk_memcpy_d2h_async": (c_int, [c_void_p, c_uint64, c_int64]),
+    "dk_stream_new": (c_int, [POINTER(c_uint64)]),
+    "dk_event_new": (c_int, [POINTER(c_uint64)]),
+    "dk_event_record": (c_int, [c_uint64]),
+    "dk_stream_wait_event": (c_int, [c_uint64]),
+    "dk_event_sync": (c_int, [c_uint64]),
+    "dk_event_elapsed_ms": (c_int, [c_uint64, c_uint64, POINTER(ctypes.c_float)]),
     "dk_kernel_compile": (c_int, [c_char_p, c_int64, POINTER(c_int64)]),
     "dk_kernel_source": (c_int, [c_int64, c_char_p, c_int64, POINTER(c_int64)]),
     "dk_kernel_num_reductions": (c_int, [c_int64, POINTER(c_int)]),
