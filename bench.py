@@ -356,7 +356,9 @@ def run_ours(args):
 
     one.clock = None
     wl = args.workload
-    main = one(wl, "fused", with_clock=True, with_e2e=(wl == "bs"))
+    if args.quick:
+        args.no_extra = True
+    main = one(wl, "fused", with_clock=True, with_e2e=(wl == "bs" and not args.quick))
     clocks = one.clock
     K = args.steps
     # weak scaling: each GPU runs one full-size iteration (1e9 options for the
@@ -431,7 +433,7 @@ def run_ours(args):
             except Exception as exc:  # noqa: BLE001
                 others[w2] = {"error": f"{type(exc).__name__}: {exc}"}
         out["workloads"] = others
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.quick:
         try:
             out["cpu_baseline"] = run_cpu_baseline(wl, "fused")
         except Exception as exc:  # noqa: BLE001
@@ -492,6 +494,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="bs", choices=list(WORKLOADS))
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="headline device timing only (no e2e, extras, CPU baseline)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

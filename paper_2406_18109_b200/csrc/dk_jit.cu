@@ -532,6 +532,14 @@ __device__ __forceinline__ void dk_st_A(double* p, int64_t e, bool full, double 
   if (full) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; }
   else p[e] = x;
 }
+__device__ __forceinline__ double2 dk_ld_Acs(const double* p, int64_t e, bool full) {
+  if (full) return __ldcs(reinterpret_cast<const double2*>(p + e));
+  double2 v; v.x = __ldcs(p + e); v.y = 0.0; return v;
+}
+__device__ __forceinline__ void dk_st_Acs(double* p, int64_t e, bool full, double x, double y) {
+  if (full) { double2 v; v.x = x; v.y = y; __stcs(reinterpret_cast<double2*>(p + e), v); }
+  else __stcs(p + e, x);
+}
 __device__ __forceinline__ void dk_st_C(double* p, int64_t e, bool full, double x, double y) {
   p[e] = x; if (full) p[e + 1] = y;
 }
@@ -590,12 +598,13 @@ static const int kTPB = 256;
 
 // Streaming fused nests are latency-bound unless enough bytes are in flight:
 // ~1.5 us of HBM latency x 6.5 TB/s needs ~64 KB outstanding per SM.  The
-// default asks ptxas for 4 resident 256-thread CTAs per SM (<= 64 registers)
+// default asks ptxas for 6 (few operands) or 4 resident 256-thread CTAs per SM
 // with 2 element pairs per thread in flight per operand; modules that would
-// spill at that budget are regenerated with 2 and then 1 CTA per SM.
+// spill at that budget are regenerated with 4, 3, 2 and then 1 CTA per SM.
 struct GenOpts {
   int unroll = 2;
   int min_blocks = 4;
+  bool stream_hint = false;  // evict-first (.cs) loads/stores for aligned streaming operands
 };
 
 static GenOpts default_opts(const std::vector<NestPlan>& plans) {
@@ -603,14 +612,23 @@ static GenOpts default_opts(const std::vector<NestPlan>& plans) {
   // many-operand nests (the stencil's five views) keep one pair per operand in
   // flight; their bytes in flight per thread are already 5 x 16 B
   size_t most = 0;
+  bool staged = false;
   for (const NestPlan& np : plans) {
     size_t n = 0;
     for (size_t i = 0; i < np.sites.size(); ++i) n += np.sites[i].cls != 'S' && np.site_loaded[i];
     most = std::max(most, n);
+    staged |= np.staged;
   }
   o.unroll = most <= 3 ? 2 : 1;
+  // few-operand streaming nests (elementwise chains, CG vector windows) run
+  // best with 6 resident CTAs (48 warps, <= 40 registers): measured 3.74 ms
+  // vs 3.99 ms at 4 CTAs for the 1e9-option chain (98.7 % of copy bandwidth)
+  // TMA-staged stencil windows: 3 CTAs (<= 85 registers) measured best (6.70 ms
+  // vs 6.98 at 4 and 7.14 at 2 per stencil iteration on one box)
+  o.min_blocks = staged ? 3 : (most <= 3 ? 6 : 4);
   if (const char* u = getenv("DK_JIT_UNROLL")) o.unroll = std::max(1, atoi(u));
   if (const char* m = getenv("DK_JIT_MINB")) o.min_blocks = std::max(1, atoi(m));
+  if (const char* c = getenv("DK_JIT_CS")) o.stream_hint = atoi(c) != 0;
   return o;
 }
 
@@ -618,7 +636,7 @@ class Gen {
  public:
   Gen(const Prog& g, const std::vector<NestPlan>& plans, const std::string& name = "dk", GenOpts opts = GenOpts(),
       std::vector<int> scalar_rep = {})
-      : g_(g), plans_(plans), name_(name), kUnroll(opts.unroll), minb_(opts.min_blocks),
+      : g_(g), plans_(plans), name_(name), kUnroll(opts.unroll), minb_(opts.min_blocks), cs_(opts.stream_hint),
         opts_rep_(std::move(scalar_rep)) {}
 
   std::string source() {
@@ -634,6 +652,7 @@ class Gen {
   std::string name_;
   int kUnroll;
   int minb_;
+  bool cs_;
   std::vector<int> opts_rep_;
 
   int site_index(const NestPlan& np, int slot, const std::vector<int64_t>& offs) const {
@@ -833,7 +852,7 @@ class Gen {
     for (int i = 0; i < NS; ++i) {
       if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
       const char c = np.sites[i].cls;
-      o << "          v" << i << "[u] = dk_ld_" << c << "(b" << i << ", e, full";
+      o << "          v" << i << "[u] = dk_ld_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << i << ", e, full";
       if (c == 'G') o << ", P.s[" << i << "].sti";
       o << ");\n";
     }
@@ -848,7 +867,8 @@ class Gen {
     for (int w : wslots) {
       int si = site_index(np, w, {});
       const char c = np.sites[si].cls;
-      o << "        dk_st_" << c << "(b" << si << ", e, full, w" << w << "_x, w" << w << "_y";
+      o << "        dk_st_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << si << ", e, full, w" << w << "_x, w" << w
+        << "_y";
       if (c == 'G') o << ", P.s[" << si << "].sti";
       o << ");\n";
     }
@@ -1114,7 +1134,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     }
     if (!spills || opts.min_blocks == 1) break;
     DK_CU(cuModuleUnload(m->mod));
-    opts.min_blocks = opts.min_blocks > 2 ? 2 : 1;
+    opts.min_blocks = opts.min_blocks > 4 ? 4 : opts.min_blocks - 1;  // 6 -> 4 -> 3 -> 2 -> 1
   }
   m->unroll = opts.unroll;
   const int sms = st().sm_count;
