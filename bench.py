@@ -28,9 +28,9 @@ import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
-# stdout carries exactly one JSON line: keep NCCL's version banner off it
-if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
-    os.environ["NCCL_DEBUG"] = "WARN"
+# stdout carries exactly one JSON line: NCCL's debug output (its "NCCL version"
+# banner at NCCL_DEBUG >= VERSION) goes to stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 WL_DIR = os.path.join(REPO, "paper_2406_18109_b200", "workloads")
 

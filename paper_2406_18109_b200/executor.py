@@ -425,11 +425,10 @@ class Executor:
 
         # access roles per argument
         if kp is None:
-            reads = [a.reads or a.reduces or (a.writes and task.kind == "OPAQUE") for a in task.args]
+            # OPAQUE adds 1.0 to its W args in place (executor.py:101-104): it reads them
+            reads = [a.reads or (a.writes and task.kind == "OPAQUE") for a in task.args]
             writes = [a.writes for a in task.args]
-            reduces = [False] * len(task.args)
-            if task.kind == "NORM":
-                reads = [a.reads or a.reduces for a in task.args]
+            reduces = [a.reduces for a in task.args]
         else:
             read_first, stored, red_slots = self._access(kp)
             reads = [False] * len(task.args)
@@ -473,7 +472,7 @@ class Executor:
 
         mine = [i for i in range(V) if prank[i] == self.rank]
         if kp is None:
-            self._run_builtin(task, pts, mine, rects, writes)
+            self._run_builtin(task, pts, mine, rects, prank)
         else:
             self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
         self.stats.launches += 1
@@ -665,19 +664,55 @@ class Executor:
                 tv = self.view(r, rect)
                 check(self.lib.dk_accum(byref(tv), gathered, idx[i][k], 1, 1))
 
-    def _run_builtin(self, task, pts, mine, rects, writes) -> None:
+    def _run_builtin(self, task, pts, mine, rects, prank) -> None:
         n = len(task.args)
         wflags = (c_int32 * max(n, 1))(*[1 if a.writes else 0 for a in task.args])
         kind = task.kind.encode()
-        if self.world > 1 and any(a.reduces for a in task.args) and len(set(self.point_rank(i, len(pts)) for i in range(len(pts)))) > 1:
-            raise UnsupportedError(f"{task.kind}: reduction builtin across several GPUs")
-        for i in mine:
+        red = [j for j, a in enumerate(task.args) if a.reduces]
+        arenas = self.world > 1 and bool(red)
+        if arenas:
+            # per-point zero arenas for the Rd args (executor.py:280-281), then the
+            # same allgather + point-order fold as kernel reductions
+            for j in red:
+                a = task.args[j]
+                if not a.part.is_none or self.shape(a.store) != ():
+                    raise UnsupportedError(f"{task.kind}: multi-GPU builtin reductions need rank-0 NonePart targets")
+            counts = [0] * self.world
+            for q in prank:
+                counts[q] += 1
+            maxp, nred = max(counts), len(red)
+            block = maxp * nred
+            tb = c_uint64()
+            check(self.lib.dk_scratch_alloc(8 * block * (self.world + 1), byref(tb)))
+            check(self.lib.dk_memset_zero(tb.value, 8 * block * (self.world + 1)))
+        for slot_in_rank, i in enumerate(mine):
             views = (dk_view * max(n, 1))()
             for j, a in enumerate(task.args):
+                if arenas and j in red:
+                    v = dk_view()
+                    v.ptr = tb.value + 8 * (block * self.rank + slot_in_rank * nred + red.index(j))
+                    v.rank, v.dtype = 0, DK_F64
+                    views[j] = v
+                    continue
                 r = self.stores[a.store]
                 self._ensure(r, rects[i][j])
                 views[j] = self.view(r, rects[i][j])
             check(self.lib.dk_builtin(kind, views, n, wflags))
+        if arenas:
+            gathered = tb.value + 8 * block
+            check(self.lib.dk_comm_allgather_f64(tb.value + 8 * block * self.rank, gathered, block))
+            seen = [0] * self.world
+            order = []
+            for q in prank:
+                order.append((q, seen[q]))
+                seen[q] += 1
+            for i, (q, s) in enumerate(order):
+                for k, j in enumerate(red):
+                    r = self.stores[task.args[j].store]
+                    self._ensure(r, r.full)
+                    tv = self.view(r, r.full)
+                    check(self.lib.dk_accum(byref(tv), gathered, (q * maxp + s) * nred + k, 1, 1))
+            check(self.lib.dk_scratch_free(tb.value))
 
     # ---------------------------------------------------------- host access
     def upload(self, sid: int, host: np.ndarray) -> None:
