@@ -365,6 +365,7 @@ class Executor:
 
     # --------------------------------------------------------------- views
     def view(self, r: StoreRec, rect) -> dk_view:
+        self._device(r)  # empty views still need a base address
         v = dk_view()
         lo, hi = rect
         off = sum(l * s for l, s in zip(lo, r.strides))
@@ -521,22 +522,30 @@ class Executor:
         return hit[1]
 
     def _check_cross_rank(self, task, prank, rects, reads, writes, temp_positions) -> None:
-        """Points of one launch on different GPUs must not exchange data."""
+        """Points of one launch on different GPUs must not need each other's data.
+
+        The reference runs points in lexicographic order (executor.py:193-195),
+        so point q observes an earlier point p's writes.  Running them
+        concurrently on different GPUs is equivalent unless q reads -- before
+        writing it itself -- a region an earlier point on another GPU writes.
+        Overlapping writes alone are fine: the later point's value is the one
+        the coherence bookkeeping keeps (``_wrote`` in point order).
+        """
         V = len(prank)
         if len(set(prank)) < 2:
             return
-        wr = [(prank[i], a.store, rects[i][j]) for i in range(V) for j, a in enumerate(task.args)
+        wr = [(i, prank[i], a.store, rects[i][j]) for i in range(V) for j, a in enumerate(task.args)
               if writes[j] and j not in temp_positions]
         if not wr:
             return
         for i in range(V):
             for j, a in enumerate(task.args):
-                if j in temp_positions or not (reads[j] or writes[j]):
+                if j in temp_positions or not reads[j]:
                     continue
-                for q, sid, w in wr:
-                    if q != prank[i] and sid == a.store and rg.overlaps(w, rects[i][j]):
+                for p, q, sid, w in wr:
+                    if p < i and q != prank[i] and sid == a.store and rg.overlaps(w, rects[i][j]):
                         raise UnsupportedError(
-                            f"{task.kind}: points on different GPUs touch store {sid} where another writes"
+                            f"{task.kind}: point {i} reads store {sid} written by point {p} on another GPU"
                         )
 
     def _hazards(self, kp: KProg, task: TaskDesc, rects_p, temp_positions) -> None:

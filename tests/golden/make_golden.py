@@ -109,8 +109,81 @@ def write(path, cases):
     print(f"wrote {path}: {len(cases)} cases")
 
 
+def edge_streams():
+    """Hand-written streams for the binding edge cases the benchmarks do not reach.
+
+    Each returns the reference's own trace events: clamped (ragged) tiles,
+    empty sub-stores (ir.py:264-267), rank-0 nests, whole-store writes by
+    several points, 2-D ragged tiles, scalar-valued reductions (kernels.py:765).
+    """
+    from diffusekit.trace import CreatePartition, CreateStore, DropRef, Flush, TaskEvent
+
+    def ident(r):
+        return (tuple(tuple(1 if i == j else 0 for j in range(r)) for i in range(r)), (0,) * r)
+
+    out = {}
+    # 1-D ragged: store 10, tile 4, launch 3 -> last tile [8, 10)
+    ev = [CreateStore(0, (10,)), CreateStore(1, (10,)), CreateStore(2, (10,)), CreateStore(3, ()), CreateStore(4, (10,))]
+    ev += [CreatePartition(i, i, "tiling", (4,), (0,), ident(1)) for i in (0, 1, 2, 4)]
+    ev += [CreatePartition(3, 3, "none")]
+    for _ in range(2):
+        ev += [TaskEvent("ADD", (3,), ((0, 0, "R"), (1, 1, "R"), (4, 4, "W"))),
+               TaskEvent("MULT", (3,), ((4, 4, "R"), (2, 2, "W")), (("s", 0.5),)),
+               TaskEvent("DOT", (3,), ((2, 2, "R"), (0, 0, "R"), (3, 3, "Rd"))),
+               TaskEvent("MAX", (3,), ((2, 2, "R"), (1, 1, "R"), (0, 0, "W"))),
+               Flush()]
+    out["edge_ragged_1d"] = ev
+    # empty sub-stores: store 6, tile 4, launch 3 -> point 2 is [6, 6)
+    ev = [CreateStore(0, (6,)), CreateStore(1, (6,)), CreateStore(2, ())]
+    ev += [CreatePartition(0, 0, "tiling", (4,), (0,), ident(1)), CreatePartition(1, 1, "tiling", (4,), (0,), ident(1)),
+           CreatePartition(2, 2, "none")]
+    for _ in range(2):
+        ev += [TaskEvent("NEG", (3,), ((0, 0, "R"), (1, 1, "W"))),
+               TaskEvent("DOT", (3,), ((1, 1, "R"), (1, 1, "R"), (2, 2, "Rd"))),
+               TaskEvent("AXPY_RATIO", (3,), ((1, 1, "R"), (0, 0, "RW"), (2, 2, "R"), (2, 2, "R"))),
+               Flush()]
+    out["edge_empty_tiles"] = ev
+    # 2-D ragged: store (5, 7), tile (2, 3), launch (3, 3)
+    ev = [CreateStore(0, (5, 7)), CreateStore(1, (5, 7)), CreateStore(2, (5, 7)), CreateStore(3, ())]
+    ev += [CreatePartition(i, i, "tiling", (2, 3), (0, 0), ident(2)) for i in range(3)]
+    ev += [CreatePartition(3, 3, "none")]
+    for _ in range(2):
+        ev += [TaskEvent("SUB", (3, 3), ((0, 0, "R"), (1, 1, "R"), (2, 2, "W"))),
+               TaskEvent("MIN", (3, 3), ((2, 2, "R"), (0, 0, "R"), (1, 1, "W"))),
+               TaskEvent("SUM", (3, 3), ((1, 1, "R"), (3, 3, "Rd"))),
+               TaskEvent("AXPY", (3, 3), ((1, 1, "R"), (0, 0, "RW")), (("w", -1.0),)),
+               Flush()]
+    out["edge_ragged_2d"] = ev
+    # rank-0 stores: FILL by every point, scalar-valued DOT/SUM (rank-0 nests), ratio reads
+    ev = [CreateStore(0, ()), CreateStore(1, ()), CreateStore(2, ()), CreateStore(3, (8,)), CreateStore(4, (8,))]
+    ev += [CreatePartition(i, i, "none") for i in range(3)]
+    ev += [CreatePartition(3, 3, "tiling", (4,), (0,), ident(1)), CreatePartition(4, 4, "tiling", (4,), (0,), ident(1))]
+    for _ in range(2):
+        ev += [TaskEvent("FILL", (2,), ((0, 0, "W"),), (("s", 3.0),)),
+               TaskEvent("DOT", (2,), ((0, 0, "R"), (0, 0, "R"), (1, 1, "Rd"))),
+               TaskEvent("SUM", (2,), ((0, 0, "R"), (2, 2, "Rd"))),
+               TaskEvent("XPBY_RATIO", (2,), ((3, 3, "R"), (4, 4, "RW"), (1, 1, "R"), (2, 2, "R"))),
+               Flush()]
+    out["edge_rank0"] = ev
+    # divisions by zero and NaN / inf propagation through min/max/neg
+    ev = [CreateStore(0, (6,)), CreateStore(1, (6,)), CreateStore(2, (6,)), CreateStore(3, (6,))]
+    ev += [CreatePartition(i, i, "tiling", (3,), (0,), ident(1)) for i in range(4)]
+    ev += [TaskEvent("FILL", (2,), ((3, 3, "W"),), (("s", 0.0),)),
+           TaskEvent("DIV", (2,), ((0, 0, "R"), (3, 3, "R"), (1, 1, "W"))),
+           TaskEvent("SUB", (2,), ((1, 1, "R"), (1, 1, "R"), (2, 2, "W"))),
+           TaskEvent("MIN", (2,), ((2, 2, "R"), (0, 0, "R"), (3, 3, "W"))),
+           TaskEvent("MAX", (2,), ((1, 1, "R"), (0, 0, "R"), (2, 2, "W"))),
+           TaskEvent("NEG", (2,), ((3, 3, "R"), (1, 1, "W"))),
+           DropRef(3), Flush()]
+    out["edge_nan_inf"] = ev
+    return out
+
+
 def main():
     bench = []
+    for name, events in edge_streams().items():
+        for cfg in ("fused", "unfused", "w2"):
+            bench.append(case_from_events(name, events, cfg))
     for name, kw in [
         ("stencil", dict(size=34, nodes=2, iters=3)),
         ("blackscholes_chain", dict(size=256, nodes=4, iters=5)),

@@ -23,7 +23,7 @@ NAMES = [
     "jacobi/fused", "cg_like/fused", "cg_like/unfused",
     "stencil_bands_n8_k2/fused", "stencil_bands_n8_k2/unfused", "stencil_bands_n6_k4/fused",
     "cg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused", "cg_csr_6x12_k4/unfused", "pcg_csr_8x8_k2/fused",
-]
+] + [f"edge_{e}/{c}" for e in ("ragged_1d", "empty_tiles", "ragged_2d", "rank0", "nan_inf") for c in ("fused", "unfused")]
 
 
 def main():

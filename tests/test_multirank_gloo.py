@@ -69,6 +69,7 @@ def _worker(rank, world, port, names, q):
                         bad.append((name, s))
         except Exception as e:  # noqa: BLE001
             bad.append((name, f"{type(e).__name__}: {e}"))
+            break  # the peer may be blocked in a collective: stop instead of desynchronising
     q.put((rank, bad, moved))
     dist.destroy_process_group()
 
@@ -80,9 +81,11 @@ def _run(names, world=2):
     procs = [ctx.Process(target=_worker, args=(r, world, port, names, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=600) for _ in procs]
+    out = [q.get(timeout=300) for _ in procs]
     for p in procs:
-        p.join(timeout=60)
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
     return sorted(out)
 
 
@@ -96,7 +99,7 @@ MULTI_POINT = [
     "cg_csr_8x8_k2/fused", "cg_csr_8x8_k2/unfused",
     "cg_csr_6x12_k4/fused", "cg_csr_6x12_k4/unfused",
     "pcg_csr_8x8_k2/fused", "pcg_csr_8x8_k2/unfused",
-]
+] + [f"edge_{e}/{c}" for e in ("ragged_1d", "empty_tiles", "ragged_2d", "rank0", "nan_inf") for c in ("fused", "unfused")]
 
 
 def test_benchmarks_two_ranks_match_reference():

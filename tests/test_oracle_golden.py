@@ -18,7 +18,7 @@ def _check(case):
 
 
 def test_bench_traces_match_reference(bench_cases):
-    assert len(bench_cases) == 30
+    assert len(bench_cases) == 45
     for case in bench_cases:
         _check(case)
 
