@@ -83,7 +83,7 @@ class HostStreamer:
                     raise UnsupportedError("host streaming needs rank-1 views of equal length")
                 n = lens.pop()
                 step = max(2, (n // self.chunks + 1) // 2 * 2)
-                recs = [ex.stores[task.args[s.arg].store] if not s.local else None for s in kp.slots]
+                recs = [ex.rec(task.args[s.arg].store) if not s.local else None for s in kp.slots]
                 for s, r, rec in zip(kp.slots, rects, recs):
                     if s.local:
                         raise UnsupportedError("host streaming does not allocate task-local buffers")
