@@ -304,6 +304,66 @@ def e2e_bs(ex, trace, steps, torch, ext_stream, world):
     return ms, 16 * n, 8 * n, ok
 
 
+def run_gpusession(steps, rank, world, local):
+    """The drop-in path: the unchanged reference front end (diffusekit, installed under
+    baseline/_ref) driving GpuSession; iterations/s include the Python analysis."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "diffusekit")):
+        return {"skipped": "reference front end not installed (baseline/_ref)"}
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, ref)
+    from diffusekit.pipeline import SessionConfig
+    from diffusekit.trace import Flush, gen_blackscholes_chain
+
+    from paper_2406_18109_b200.session import GpuSession
+
+    n_it = 4 + 3 + steps
+    events = gen_blackscholes_chain(size=1_000_000_000 * world, nodes=world, iters=n_it)
+    its, cur = [], []
+    for ev in events:
+        cur.append(ev)
+        if isinstance(ev, Flush):
+            its.append(cur)
+            cur = []
+    s = GpuSession(SessionConfig(), rank=rank, world=world, device=local)
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [s.executor.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        s.executor.init_comm(obj[0])
+
+    def feed(evs):
+        from diffusekit.pipeline import task_from_event
+        from diffusekit.trace import CreatePartition, CreateStore, DropRef, TaskEvent, partition_from_event
+
+        for ev in evs:
+            if isinstance(ev, CreateStore):
+                s.create_store(ev.id, ev.shape)
+            elif isinstance(ev, CreatePartition):
+                s.create_partition(ev.id, partition_from_event(ev))
+            elif isinstance(ev, TaskEvent):
+                s.submit(task_from_event(s, ev))
+            elif isinstance(ev, DropRef):
+                s.drop_ref(ev.store)
+            elif isinstance(ev, Flush):
+                s.flush()
+
+    try:
+        feed([e for it in its[: n_it - steps] for e in it])
+        s.executor.sync()
+        t0 = time.perf_counter()
+        feed([e for it in its[n_it - steps:] for e in it])
+        s.executor.sync()
+        dt = time.perf_counter() - t0
+        return {"value": round(world * steps / dt, 3), "unit": "iter/s",
+                "ms_per_step": round(dt / steps * 1e3, 3),
+                "note": "wall clock: reference front end (window analysis, memo replay) + GpuSession execution; "
+                        "device time per step is ms_per_step of the headline"}
+    finally:
+        s.executor.close()
+
+
 def run_ours(args):
     import torch
 
@@ -433,6 +493,11 @@ def run_ours(args):
             except Exception as exc:  # noqa: BLE001
                 others[w2] = {"error": f"{type(exc).__name__}: {exc}"}
         out["workloads"] = others
+    if wl == "bs" and not args.no_extra:
+        try:
+            out["gpusession"] = run_gpusession(args.steps, rank, world, local)
+        except Exception as exc:  # noqa: BLE001
+            out["gpusession"] = {"error": f"{type(exc).__name__}: {exc}"}
     if rank == 0 and world == 1 and not args.quick:
         try:
             out["cpu_baseline"] = run_cpu_baseline(wl, "fused")
