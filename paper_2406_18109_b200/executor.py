@@ -108,6 +108,7 @@ class Executor:
         self._kval: dict[KProg, tuple[int, int]] = {}
         self._scal: dict[tuple, ctypes.Array] = {}
         self._acc: dict[int, tuple] = {}
+        self._plans: dict[tuple, tuple] = {}  # launch-plan cache (one GPU)
         self.stats = LaunchStats()
         self._comm = False
 
@@ -416,6 +417,22 @@ class Executor:
         if kp is None and task.kind not in BUILTIN_KINDS:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
+        if kp is not None and self.world == 1:
+            # key on the non-temporary arguments: each memo replay of a window names fresh
+            # temporaries, which never reach the device
+            pkey = (id(kp), task.launch, temp_positions, task.scalars,
+                    tuple(a for j, a in enumerate(task.args) if j not in temp_positions))
+            hit = self._plans.get(pkey)
+            # valid while every store is the same record: on one GPU a store's valid
+            # region only grows until it is freed, and bindings depend only on shapes
+            if hit is not None and hit[0] is kp and all(self.stores.get(s) is r for s, r in hit[1]):
+                h, _ = self.kernel_handle(kp)
+                scal = self._scalars(task.scalars)
+                for views in hit[2]:
+                    check(self.lib.dk_launch(h, views, len(kp.slots), scal, len(task.scalars), 0))
+                self.stats.launches += 1
+                self.stats.points += len(hit[2])
+                return
         pts = list(task.points())
         V = len(pts)
         prank = [self.point_rank(i, V) for i in range(V)]
@@ -475,7 +492,15 @@ class Executor:
         if kp is None:
             self._run_builtin(task, pts, mine, rects, prank)
         else:
-            self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
+            recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
+            if recorded is not None and self.world == 1:
+                # launch-plan cache: a memo-replayed window over the same
+                # stores re-launches with the bound views as they are
+                if len(self._plans) > 4096:
+                    self._plans.clear()
+                recs = tuple((a.store, self.stores[a.store]) for j, a in enumerate(task.args)
+                             if j not in temp_positions)
+                self._plans[pkey] = (kp, recs, recorded)
         self.stats.launches += 1
         self.stats.points += len(mine)
 
@@ -589,8 +614,10 @@ class Executor:
             check(self.lib.dk_scratch_alloc(nbytes * (self.world + 1), byref(tb)))
             totals = tb.value
             check(self.lib.dk_memset_zero(totals, nbytes * (self.world + 1)))
-        views = (dk_view * nslots)()
+        has_local = any(s.local for s in kp.slots)
+        recorded = [] if not (use_totals or has_local) else None
         for slot_in_rank, i in enumerate(mine):
+            views = (dk_view * nslots)()
             rp = rects[i]
             self._hazards(kp, task, rp, temp_positions)
             scratch = []
@@ -622,9 +649,12 @@ class Executor:
             check(self.lib.dk_launch(h, views, nslots, scal, len(task.scalars), tot))
             for p in scratch:
                 check(self.lib.dk_scratch_free(p))
+            if recorded is not None:
+                recorded.append(views)
         if use_totals:
             self._fold(task, kp, prank, rects, red_targets, totals, maxp, nred)
             check(self.lib.dk_scratch_free(totals))
+        return recorded
 
     def _fold(self, task, kp, prank, rects, red_targets, totals, maxp, nred) -> None:
         """All-gather per-point totals; fold in lexicographic point order."""

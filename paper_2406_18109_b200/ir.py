@@ -92,6 +92,13 @@ class TaskDesc:
         """Launch points in lexicographic order (ir.py:46-48)."""
         return itertools.product(*(range(e) for e in self.launch))
 
+    def __hash__(self) -> int:  # cached: fused tasks carry dozens of arguments
+        h = self.__dict__.get("_hash")
+        if h is None:
+            h = hash((self.kind, self.launch, self.args, self.scalars, self.scalar_names))
+            object.__setattr__(self, "_hash", h)
+        return h
+
     @property
     def volume(self) -> int:
         v = 1
