@@ -385,8 +385,8 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if peaks else "fallback"
 
-    def one(wl, mode, with_clock=False, with_e2e=False):
-        trace = load_trace(f"{wl}_{mode}_n{world}")
+    def one(wl, mode, with_clock=False, with_e2e=False, plan=None, steps=None):
+        trace = load_trace(plan or f"{wl}_{mode}_n{world}")
         ex = make_executor(trace, rank, world, local, torch)
         ext = torch.cuda.ExternalStream(ex.stream())
         sampler = ClockSampler(local) if with_clock else None
@@ -397,7 +397,7 @@ def run_ours(args):
             barrier(torch, world)
             if sampler:
                 sampler.mark("t0")
-            ms, launches, dom, it_bytes = measure(ex, trace, args.steps, args.warmup, torch, ext, rank)
+            ms, launches, dom, it_bytes = measure(ex, trace, steps or args.steps, args.warmup, torch, ext, rank)
             if sampler:
                 sampler.mark("t1")
             ms = reduce_max(torch, world, ms)
@@ -493,6 +493,15 @@ def run_ours(args):
             except Exception as exc:  # noqa: BLE001
                 others[w2] = {"error": f"{type(exc).__name__}: {exc}"}
         out["workloads"] = others
+        if world == 1:
+            # BASELINE configs[0]: the reference's own case (1M options, one partition)
+            try:
+                c1 = one("bs", "fused", plan="bs_fused_c1", steps=200)
+                out["c1_1M_options"] = {"fused_iter_s": round(200 / (c1["ms"] / 1e3), 1),
+                                        "ms_per_step": round(c1["ms"] / 200, 4),
+                                        "note": "device-timed 200 replayed iterations; host enqueue bound at this size"}
+            except Exception as exc:  # noqa: BLE001
+                out["c1_1M_options"] = {"error": f"{type(exc).__name__}: {exc}"}
     if wl == "bs" and not args.no_extra:
         try:
             out["gpusession"] = run_gpusession(args.steps, rank, world, local)
