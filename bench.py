@@ -127,10 +127,19 @@ class ClockSampler:
 
 
 def run_cpu_baseline(wl, mode, budget_s=10.0):
-    """The oracle port of the reference executor on the bounded CPU sample (rank 0, N=1)."""
+    """The reference's CPU path on a bounded sample (rank 0, N=1): the unmodified
+    reference when it is installed (Black-Scholes), else the oracle port."""
+    desc, cpu_name, full_units, cpu_units = WORKLOADS[wl]
+    if wl == "bs" and mode == "fused":
+        got = reference_session_rate(int(cpu_units), budget_s)
+        if got is not None:
+            its_s, n, dt = got
+            return {"value": its_s * cpu_units / full_units, "unit": "iter/s", "cores": 1, "kind": "reference",
+                    "sample": f"{n} steady iterations of the unmodified diffusekit.Session (baseline/_ref) on "
+                              f"gen_blackscholes_chain({int(cpu_units):,} options) in {dt:.1f}s = {its_s:.3f} it/s, "
+                              f"scaled linearly to {int(full_units):,} (numpy ufunc loops are single-threaded)"}
     from oracle.interp import replay as oreplay
 
-    desc, cpu_name, full_units, cpu_units = WORKLOADS[wl]
     tr = load_trace(cpu_name.format(mode=mode))
     its, steady = iteration_split(tr)
     heap = None
@@ -155,6 +164,55 @@ def run_cpu_baseline(wl, mode, budget_s=10.0):
         "sample": f"{n} steady iterations of {cpu_name.format(mode=mode)} ({int(cpu_units):,} units) in {dt:.1f}s "
                   f"= {its_s:.3f} it/s, scaled linearly to {int(full_units):,} units (numpy ufuncs are single-threaded)",
     }
+
+
+def reference_session_rate(size, budget_s=None, warmup=3, steps=None):
+    """Time steady iterations of the unmodified reference Session (numpy executor).
+
+    Returns (iter/s, iterations, seconds) or None when the reference is not installed."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "diffusekit")):
+        return None
+    sys.dont_write_bytecode = True
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from diffusekit.pipeline import Session, SessionConfig, task_from_event
+    from diffusekit.trace import CreatePartition, CreateStore, DropRef, Flush, TaskEvent, \
+        gen_blackscholes_chain, partition_from_event
+
+    cap = steps or 200
+    n_it = 4 + warmup + cap
+    s = Session(SessionConfig())
+    its, cur = [], []
+    for ev in gen_blackscholes_chain(size=size, nodes=1, iters=n_it):
+        cur.append(ev)
+        if isinstance(ev, Flush):
+            its.append(cur)
+            cur = []
+
+    def feed(evs):
+        for ev in evs:
+            if isinstance(ev, CreateStore):
+                s.create_store(ev.id, ev.shape)
+            elif isinstance(ev, CreatePartition):
+                s.create_partition(ev.id, partition_from_event(ev))
+            elif isinstance(ev, TaskEvent):
+                s.submit(task_from_event(s, ev))
+            elif isinstance(ev, DropRef):
+                s.drop_ref(ev.store)
+            else:
+                s.flush()
+
+    feed([e for it in its[: 4 + warmup] for e in it])
+    t0 = time.perf_counter()
+    n = 0
+    for it in its[4 + warmup:]:
+        feed(it)
+        n += 1
+        if (steps and n >= steps) or (budget_s and time.perf_counter() - t0 >= budget_s):
+            break
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
 
 
 def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True):
@@ -527,19 +585,27 @@ def run_reference(args):
     wl = args.workload
     desc, cpu_name, full_units, cpu_units = WORKLOADS[wl]
     K, W = args.steps, args.warmup
-    from oracle.interp import replay as oreplay
+    dt, kind, what = None, "port", cpu_name.format(mode="fused")
+    got = reference_session_rate(int(cpu_units), warmup=W, steps=K) if wl == "bs" else None
+    if got is not None:
+        # the unmodified reference itself: diffusekit Session + numpy executor on the
+        # 1M-option chain (its own CPU configuration), front-end analysis included
+        dt = got[2]
+        kind, what = "reference", "diffusekit.Session (unmodified, baseline/_ref) on gen_blackscholes_chain"
+    if dt is None:
+        from oracle.interp import replay as oreplay
 
-    tr = load_trace(cpu_name.format(mode="fused"))
-    its, steady = iteration_split(tr)
-    heap = None
-    for it in its[: steady + W]:
-        heap = oreplay(tr, it, heap)
-    t0 = time.perf_counter()
-    i = steady + W
-    for _ in range(K):
-        heap = oreplay(tr, its[i], heap)
-        i = i + 1 if i + 1 < len(its) else steady
-    dt = time.perf_counter() - t0
+        tr = load_trace(cpu_name.format(mode="fused"))
+        its, steady = iteration_split(tr)
+        heap = None
+        for it in its[: steady + W]:
+            heap = oreplay(tr, it, heap)
+        t0 = time.perf_counter()
+        i = steady + W
+        for _ in range(K):
+            heap = oreplay(tr, its[i], heap)
+            i = i + 1 if i + 1 < len(its) else steady
+        dt = time.perf_counter() - t0
     v = K / dt * cpu_units / full_units
     print(json.dumps({
         "impl": "reference",
@@ -553,9 +619,10 @@ def run_reference(args):
         "scaling": "weak",
         "dtype": "f64",
         "config": {"workload": desc, "mode": "fused"},
-        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "port",
-                         "sample": f"{K} steady iterations of {cpu_name.format(mode='fused')} ({int(cpu_units):,} "
-                                   f"units, {dt / K * 1e3:.1f} ms/iter) scaled to {int(full_units):,} units"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": kind,
+                         "sample": f"{K} steady iterations of {what} ({int(cpu_units):,} "
+                                   f"units, {dt / K * 1e3:.1f} ms/iter) scaled to {int(full_units):,} units "
+                                   f"(numpy ufunc loops are single-threaded)"},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
