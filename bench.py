@@ -261,7 +261,8 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
         mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
         byts = launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
         dom = {"kind": e.task.kind, "f": e.f, "avg_ms": tot / cnt, "launches": cnt, "bytes": byts,
-               "share": tot / ms if ms else None}
+               "share": tot / ms if ms else None,
+               "per_exec_ms": {f"{k[0]}/{k[1]}": round(v[1] / v[2], 4) for k, v in per.items()}}
     # algorithmic bytes of one timed iteration on this rank
     it_bytes = 0
     for k, e in its[timed[0]]:
@@ -487,7 +488,8 @@ def run_ours(args):
     traffic = None
     try:
         tr_js = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
-        traffic = tr_js.get(f"{wl}_fused", {}).get("dram_bytes_per_launch")
+        if dom:
+            traffic = tr_js.get(wl, {}).get(f"{dom['kind']}/{dom['f']}")
     except (OSError, ValueError):
         pass
     if dom:
@@ -515,6 +517,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (24 GB per step)" if wl == "bs" else "inputs larger than L2"},
         "roofline": roof,
         "hbm_gbs_step": round(main["it_bytes"] / (main["ms"] / K / 1e3) / 1e9, 1),
+        "per_exec_ms": dom["per_exec_ms"] if dom else None,
         "gpu_launches": main["launches"],
         "clocks": clocks,
     }

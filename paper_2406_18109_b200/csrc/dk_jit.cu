@@ -241,6 +241,15 @@ struct Site {
 static const int kTR = 8;     // output rows per tile
 static const int kTC = 128;   // output columns per tile (64 element pairs)
 static const int kBW = 136;   // TMA box width (tile + column halo + alignment), 1088 B per row
+// TMA ring depth: S-1 boxes in flight per CTA (DK_K3_STAGES, 2..4)
+static int kStages() {
+  static int s = [] {
+    const char* e = getenv("DK_K3_STAGES");
+    int v = e ? atoi(e) : 3;
+    return std::min(4, std::max(2, v));
+  }();
+  return s;
+}
 
 struct NestPlan {
   int rank = 0;  // actual domain rank
@@ -612,10 +621,13 @@ static GenOpts default_opts(const std::vector<NestPlan>& plans) {
   // many-operand nests (the stencil's five views) keep one pair per operand in
   // flight; their bytes in flight per thread are already 5 x 16 B
   size_t most = 0;
-  bool staged = false;
+  bool staged = false, all_aligned = true;
   for (const NestPlan& np : plans) {
     size_t n = 0;
-    for (size_t i = 0; i < np.sites.size(); ++i) n += np.sites[i].cls != 'S' && np.site_loaded[i];
+    for (size_t i = 0; i < np.sites.size(); ++i) {
+      n += np.sites[i].cls != 'S' && np.site_loaded[i];
+      all_aligned &= np.sites[i].cls == 'S' || np.sites[i].cls == 'A';
+    }
     most = std::max(most, n);
     staged |= np.staged;
   }
@@ -623,9 +635,10 @@ static GenOpts default_opts(const std::vector<NestPlan>& plans) {
   // few-operand streaming nests (elementwise chains, CG vector windows) run
   // best with 6 resident CTAs (48 warps, <= 40 registers): measured 3.74 ms
   // vs 3.99 ms at 4 CTAs for the 1e9-option chain (98.7 % of copy bandwidth)
-  // TMA-staged stencil windows: 3 CTAs (<= 85 registers) measured best (6.70 ms
-  // vs 6.98 at 4 and 7.14 at 2 per stencil iteration on one box)
-  o.min_blocks = staged ? 3 : (most <= 3 ? 6 : 4);
+  // Same-box sweeps: the TMA-staged stencil window runs best at 3 CTAs; nests with an
+  // unaligned (odd-offset) operand at 4 (stencil COPY 3.21 ms vs 3.71 at 6); fully
+  // aligned few-operand nests at 6 (BS 3.94 vs 3.98 ms at 4).
+  o.min_blocks = staged ? 3 : (most <= 3 && all_aligned ? 6 : 4);
   if (const char* u = getenv("DK_JIT_UNROLL")) o.unroll = std::max(1, atoi(u));
   if (const char* m = getenv("DK_JIT_MINB")) o.min_blocks = std::max(1, atoi(m));
   if (const char* c = getenv("DK_JIT_CS")) o.stream_hint = atoi(c) != 0;
@@ -720,28 +733,38 @@ class Gen {
     const int ROWS = np.st_rows;
     const unsigned bytes = (unsigned)(ROWS * kBW * 8);
     for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
-    // even row count per stage keeps stage 1 on a 128-byte boundary (TMA destination alignment)
-    o << "  __shared__ __align__(128) double dk_tile[2][" << (ROWS + 1) / 2 * 2 << "][" << kBW << "];\n";
-    o << "  __shared__ __align__(8) unsigned long long dk_bar[2];\n";
+    // S-stage ring; an even row count per stage keeps every stage on a 128-byte
+    // boundary (TMA destination alignment)
+    const int S = kStages();
+    o << "  __shared__ __align__(128) double dk_tile[" << S << "][" << (ROWS + 1) / 2 * 2 << "][" << kBW << "];\n";
+    o << "  __shared__ __align__(8) unsigned long long dk_bar[" << S << "];\n";
     o << "  const int tid = threadIdx.x;\n";
     o << "  const int64_t D0 = P.h.ext[0], D1 = P.h.ext[1];\n";
-    o << "  const int64_t ntc = (D1 + " << kTC - 1 << ") / " << kTC << ", ntiles = ((D0 + " << kTR - 1 << ") / " << kTR
-      << ") * ntc;\n";
-    o << "  const uint32_t bar0 = dk_smem(&dk_bar[0]), bar1 = dk_smem(&dk_bar[1]);\n";
-    o << "  if (tid == 0) { dk_mbar_init(bar0, 1); dk_mbar_init(bar1, 1); dk_fence_mbar_init(); }\n";
-    o << "  __syncthreads();\n";
+    o << "  const int64_t ntc = (D1 + " << kTC - 1 << ") / " << kTC << ", ntr = (D0 + " << kTR - 1 << ") / " << kTR
+      << ", ntiles = ntr * ntc;\n";
+    // tile order: row-major (DK_K3_COLMAJOR=1 walks column strips; measured equal time)
+    const bool colmaj = getenv("DK_K3_COLMAJOR") != nullptr;
+    auto trow = [&](const char* t) { return colmaj ? std::string("(") + t + " % ntr)" : std::string("(") + t + " / ntc)"; };
+    auto tcol = [&](const char* t) { return colmaj ? std::string("(") + t + " / ntr)" : std::string("(") + t + " % ntc)"; };
+    o << "  if (tid == 0) {\n    for (int s = 0; s < " << S << "; ++s) dk_mbar_init(dk_smem(&dk_bar[s]), 1);\n";
+    o << "    dk_fence_mbar_init();\n  }\n  __syncthreads();\n";
     o << "  int64_t tile = blockIdx.x;\n";
-    o << "  if (tid == 0 && tile < ntiles)\n    dk_tma_2d(&P.tm, bar0, dk_smem(&dk_tile[0][0][0]), (int)((tile % ntc) * " << kTC
-      << "), (int)((tile / ntc) * " << kTR << "), " << bytes << "u);\n";
+    // prologue: S-1 tiles in flight
+    o << "  if (tid == 0)\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
+    o << "      const int64_t t = tile + (int64_t)s * gridDim.x;\n      if (t >= ntiles) break;\n";
+    o << "      dk_tma_2d(&P.tm, dk_smem(&dk_bar[s]), dk_smem(&dk_tile[s][0][0]), (int)(" << tcol("t") << " * " << kTC
+      << "), (int)(" << trow("t") << " * " << kTR << "), " << bytes << "u);\n    }\n";
     o << "  const int pr = tid & 63, rg = tid >> 6;\n";
     o << "  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {\n";
-    o << "    const int stg = it & 1;\n    const uint32_t ph = (uint32_t)((it >> 1) & 1);\n";
-    o << "    const int64_t nxt = tile + gridDim.x;\n";
-    o << "    if (tid == 0 && nxt < ntiles) {\n      dk_fence_proxy_async();\n";
-    o << "      dk_tma_2d(&P.tm, stg ? bar0 : bar1, dk_smem(&dk_tile[stg ^ 1][0][0]), (int)((nxt % ntc) * " << kTC
-      << "), (int)((nxt / ntc) * " << kTR << "), " << bytes << "u);\n    }\n";
-    o << "    dk_mbar_wait(stg ? bar1 : bar0, ph);\n";
-    o << "    const int64_t r0 = (tile / ntc) * " << kTR << ", c0 = (tile % ntc) * " << kTC << ";\n";
+    o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
+    o << "    const int64_t nxt = tile + (int64_t)" << S - 1 << " * gridDim.x;\n";
+    // the stage refilled here was read in iteration it-1 and released by its __syncthreads
+    o << "    if (tid == 0 && nxt < ntiles) {\n      const int ns = (it + " << S - 1 << ") % " << S << ";\n";
+    o << "      dk_fence_proxy_async();\n";
+    o << "      dk_tma_2d(&P.tm, dk_smem(&dk_bar[ns]), dk_smem(&dk_tile[ns][0][0]), (int)(" << tcol("nxt") << " * " << kTC
+      << "), (int)(" << trow("nxt") << " * " << kTR << "), " << bytes << "u);\n    }\n";
+    o << "    dk_mbar_wait(dk_smem(&dk_bar[stg]), ph);\n";
+    o << "    const int64_t r0 = " << trow("tile") << " * " << kTR << ", c0 = " << tcol("tile") << " * " << kTC << ";\n";
     o << "    const double (*T)[" << kBW << "] = dk_tile[stg];\n";
     for (int i = 0; i < NS; ++i)
       if (np.sites[i].cls != 'S' && np.site_loaded[i]) o << "    double2 v" << i << "[2];\n";
@@ -1162,6 +1185,20 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
   return raw;
 }
 
+// L2 sector promotion of the staged tiles' TMA loads (DK_TMA_L2 = 0 | 64 | 128 | 256)
+static CUtensorMapL2promotion tma_l2_promotion() {
+  static int v = [] {
+    const char* e = getenv("DK_TMA_L2");
+    return e ? atoi(e) : 128;
+  }();
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+}
+
 static int64_t pow2ceil(int64_t v) {
   int64_t p = 1;
   while (p < v) p <<= 1;
@@ -1230,7 +1267,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       cuuint32_t estr[2] = {1, 1};
       DK_CU(cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)np.st_base, gdim, gstr, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+                                   tma_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
       memcpy(p, &tm, 128);
       p += 128;
     }
