@@ -148,12 +148,29 @@ def _part_from_ref(part: Any) -> PartDesc:
     return NONE_PART
 
 
+_PART_CACHE: dict[Any, PartDesc] = {}
+
+
+def _part_cached(part: Any) -> PartDesc:
+    # reference partitions are frozen (hash/eq by value); a fused window lowers
+    # dozens of identical tilings every iteration
+    try:
+        hit = _PART_CACHE.get(part)
+    except TypeError:
+        return _part_from_ref(part)
+    if hit is None:
+        if len(_PART_CACHE) > 100_000:
+            _PART_CACHE.clear()
+        hit = _PART_CACHE[part] = _part_from_ref(part)
+    return hit
+
+
 def lower_task(task: Any) -> TaskDesc:
     """Reference ``IndexTask`` (ir.py:172-190) -> :class:`TaskDesc`."""
     if isinstance(task, TaskDesc):
         return task
     args = tuple(
-        ArgDesc(int(a.store), _part_from_ref(a.partition), a.privilege.value) for a in task.args
+        ArgDesc(int(a.store), _part_cached(a.partition), a.privilege.value) for a in task.args
     )
     return TaskDesc(
         task.kind,
