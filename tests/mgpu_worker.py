@@ -26,6 +26,39 @@ NAMES = [
 ] + [f"edge_{e}/{c}" for e in ("ragged_1d", "empty_tiles", "ragged_2d", "rank0", "nan_inf") for c in ("fused", "unfused")]
 
 
+def gpusession_drop_in(rank, world, local):
+    """GpuSession (reference front end + this backend) on `world` GPUs vs the reference Session on CPU."""
+    ref = os.path.join(os.path.dirname(HERE), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "diffusekit")):
+        return []
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, ref)
+    from diffusekit.pipeline import Session, SessionConfig, run_events
+    from diffusekit.trace import gen_benchmark
+
+    from paper_2406_18109_b200.session import GpuSession
+
+    bad = []
+    for name, kw in [("cg_like", dict(size=64, nodes=world * 2, iters=4)),
+                     ("blackscholes_chain", dict(size=4096 * world, nodes=world, iters=5)),
+                     ("jacobi", dict(size=32, nodes=world, iters=3))]:
+        s = GpuSession(SessionConfig(), rank=rank, world=world, device=local)
+        s.executor._comm = True  # communicator already initialised in this process
+        rep = run_events(s, gen_benchmark(name, **kw))
+        got = {sid: s.heap.get(sid) for sid in s.live_store_ids()}
+        s.executor.close()
+        if rank == 0:
+            r = Session(SessionConfig())
+            rep_ref = run_events(r, gen_benchmark(name, **kw))
+            if rep.fused_prefixes != rep_ref.fused_prefixes:
+                bad.append((f"gpusession/{name}", "plan"))
+            for sid, g in got.items():
+                w = r.heap.get(sid)
+                if not (same_bits(g, w) or np.allclose(g, w, rtol=1e-12, atol=1e-12 * max(1.0, float(np.abs(w).max())))):
+                    bad.append((f"gpusession/{name}", sid))
+    return bad
+
+
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -60,6 +93,7 @@ def main():
                     close += 1
                 else:
                     bad.append((name, s))
+    bad += gpusession_drop_in(rank, world, local)
     if rank == 0:
         print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved}")
         if bad:
