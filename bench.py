@@ -460,7 +460,8 @@ def run_ours(args):
             if sampler:
                 sampler.mark("t1")
             ms = reduce_max(torch, world, ms)
-            res = {"ms": ms, "launches": launches, "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats)}
+            res = {"ms": ms, "launches": launches, "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats),
+                   "jit": ex.jit_stats()}
             if with_e2e:
                 e_ms, bi, bo, ok = e2e_bs(ex, trace, args.steps, torch, ext, world)
                 res["e2e"] = (reduce_max(torch, world, e_ms), bi, bo, ok)
@@ -519,6 +520,7 @@ def run_ours(args):
         "hbm_gbs_step": round(main["it_bytes"] / (main["ms"] / K / 1e3) / 1e9, 1),
         "per_exec_ms": dom["per_exec_ms"] if dom else None,
         "gpu_launches": main["launches"],
+        "jit": main["jit"],
         "clocks": clocks,
     }
     if "e2e" in main:

@@ -114,6 +114,9 @@ int dk_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 int dk_kernel_compile(const char* program, int64_t len, int64_t* handle);
 int dk_kernel_source(int64_t handle, char* buf, int64_t cap, int64_t* len);
 int dk_kernel_num_reductions(int64_t handle, int* n);
+/* JIT totals: modules built (one per kernel x binding class), NVRTC compiles,
+ * on-disk cubin cache hits (DK_JIT_CACHE), seconds spent in NVRTC */
+int dk_jit_stats(int64_t* modules, int64_t* compiles, int64_t* disk_hits, double* seconds);
 /* Device-free code generation (and optional NVRTC compile) for a binding:
  * returns the generated CUDA source.  Used by the CPU test-suite. */
 int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, int nviews,

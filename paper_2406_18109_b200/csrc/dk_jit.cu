@@ -32,6 +32,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <fstream>
 #include <functional>
@@ -1044,6 +1045,10 @@ static std::string cache_dir() {
   return std::string(home ? home : "/tmp") + "/.cache/dk_b200_jit";
 }
 
+// JIT statistics (dk_jit_stats): modules built, NVRTC compiles, disk-cache hits, compile seconds
+static int64_t g_jit_modules = 0, g_jit_compiles = 0, g_jit_disk_hits = 0;
+static double g_jit_seconds = 0.0;
+
 static std::string compile_cubin(const std::string& src, std::string* log_out) {
   static const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-lineinfo", "--std=c++17",
                                "-default-device"};
@@ -1060,9 +1065,19 @@ static std::string compile_cubin(const std::string& src, std::string* log_out) {
       std::stringstream ss;
       ss << f.rdbuf();
       std::string bin = ss.str();
-      if (!bin.empty()) return bin;
+      if (!bin.empty()) {
+        g_jit_disk_hits++;
+        return bin;
+      }
     }
   }
+  struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Timer() {
+      g_jit_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      g_jit_compiles++;
+    }
+  } timer;
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "dk_fused.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     fail(DK_ERR_NVRTC, "nvrtcCreateProgram failed");
@@ -1171,6 +1186,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     opts.min_blocks = opts.min_blocks > 4 ? 4 : opts.min_blocks - 1;  // 6 -> 4 -> 3 -> 2 -> 1
   }
   m->unroll = opts.unroll;
+  g_jit_modules++;
   const int sms = st().sm_count;
   for (size_t n = 0; n < k.prog.nests.size(); ++n) {
     CUfunction f = fns[n];
@@ -1407,6 +1423,15 @@ int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, in
       memcpy(buf, src.data(), (size_t)n);
       buf[n] = 0;
     }
+  });
+}
+
+int dk_jit_stats(int64_t* modules, int64_t* compiles, int64_t* disk_hits, double* seconds) {
+  return guard([&] {
+    *modules = g_jit_modules;
+    *compiles = g_jit_compiles;
+    *disk_hits = g_jit_disk_hits;
+    *seconds = g_jit_seconds;
   });
 }
 

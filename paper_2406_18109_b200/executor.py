@@ -809,6 +809,13 @@ class Executor:
     def sync(self) -> None:
         check(self.lib.dk_sync())
 
+    def jit_stats(self) -> dict:
+        m, c, d = c_int64(), c_int64(), c_int64()
+        s = c_double()
+        check(self.lib.dk_jit_stats(byref(m), byref(c), byref(d), byref(s)))
+        return {"modules": m.value, "nvrtc_compiles": c.value, "disk_cache_hits": d.value,
+                "nvrtc_seconds": round(s.value, 3)}
+
     def launch_count(self) -> int:
         n = c_int64()
         check(self.lib.dk_launch_count(byref(n)))

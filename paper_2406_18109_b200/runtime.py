@@ -82,6 +82,7 @@ _SIGS = {
     "dk_kernel_compile": (c_int, [c_char_p, c_int64, POINTER(c_int64)]),
     "dk_kernel_source": (c_int, [c_int64, c_char_p, c_int64, POINTER(c_int64)]),
     "dk_kernel_num_reductions": (c_int, [c_int64, POINTER(c_int)]),
+    "dk_jit_stats": (c_int, [POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
     "dk_kernel_codegen": (
         c_int,
         [c_char_p, c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_char_p, c_int64, POINTER(c_int64)],
