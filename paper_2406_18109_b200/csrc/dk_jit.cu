@@ -230,7 +230,8 @@ static_assert(sizeof(dk_view) == 80, "dk_view layout");
 struct Site {
   int slot;
   std::vector<int64_t> offs;  // empty = zero offsets
-  char cls;                   // S scalar, C contiguous inner, B broadcast inner, G strided inner
+  char cls;                   // S scalar, A aligned contiguous, C contiguous inner, B broadcast inner, G strided inner
+  int par = -1;               // contiguous with even row strides: element parity of the view origin
   bool staged = false;        // read through the CTA's TMA-staged tile (K3)
   int dr = 0, dc = 0;         // element offset of this view within the staged tile
 };
@@ -254,6 +255,7 @@ static int kStages() {
 
 struct NestPlan {
   int rank = 0;  // actual domain rank
+  int shift = 0;  // 1: element pairs start at column -1 (aligns the odd-parity views)
   bool staged = false;
   int st_rows = 0;         // box rows = kTR + max dr
   int st_sh = 0;           // column shift that 16-byte aligns the tensor base
@@ -406,10 +408,12 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
           // 'A': every row's element pairs are 16-byte aligned -> LDG.E.128 / STG.E.128
           int64_t shift = 0;
           for (size_t d = 0; d < o.size(); ++d) shift += o[d] * v.stride[d];
-          bool al = ((v.ptr + 8ull * (uint64_t)shift) % 16) == 0;
+          const uint64_t a = v.ptr + 8ull * (uint64_t)shift;
+          bool even = a % 8 == 0;
           for (int d = 0; d + 1 < r; ++d)
-            if (str[d] % 2) al = false;
-          if (al) s.cls = 'A';
+            if (str[d] % 2) even = false;
+          if (even) s.par = (int)((a / 8) % 2);
+          if (s.par == 0) s.cls = 'A';
         }
       }
       if (!o.empty()) {
@@ -473,7 +477,23 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
       if (r == 0 && s.cls != 'S') fail(DK_ERR_UNSUPPORTED, "rank-0 nest over an array operand");
     }
     plan_staging(np, views, D, r, kstored);
-    ks << "n" << n << ":r" << r << ":";
+    if (!np.staged && r > 0 && !getenv("DK_JIT_NO_SHIFT")) {
+      // pick the pair grid (start column 0 or -1) that 16-byte aligns the most
+      // operands; the others move as shuffled pairs ('H')
+      int score[2] = {0, 0};
+      for (size_t i = 0; i < np.sites.size(); ++i) {
+        const Site& st = np.sites[i];
+        if (st.par < 0) continue;
+        score[st.par] += (np.site_loaded[i] ? 1 : 0) + (st.offs.empty() && stored.count(st.slot) ? 1 : 0);
+      }
+      if (score[1] > score[0]) np.shift = 1;
+      // 'H' (shuffled odd-parity pairs) is opt-in: measured slower than split
+      // 8-byte accesses for the stencil COPY (3.39 vs 3.22 ms)
+      const bool useH = getenv("DK_JIT_H") != nullptr;
+      for (Site& st : np.sites)
+        if (st.cls == 'A' || st.cls == 'C') st.cls = st.par < 0 ? 'C' : st.par == np.shift ? 'A' : useH ? 'H' : 'C';
+    }
+    ks << "n" << n << ":r" << r << ":h" << np.shift << ":";
     if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
@@ -524,37 +544,43 @@ __device__ __forceinline__ double dk_bits(unsigned long long b) { return __longl
 
 // element-pair access, specialised per site class at code generation time:
 //   A aligned contiguous (one 16-byte access), C contiguous (two 8-byte),
-//   B broadcast inner dim (one load), G strided inner dim
-__device__ __forceinline__ double2 dk_ld_A(const double* p, int64_t e, bool full) {
-  if (full) return *reinterpret_cast<const double2*>(p + e);
-  double2 v; v.x = p[e]; v.y = 0.0; return v;
+//   B broadcast inner dim (one load), G strided inner dim.
+// lo / hi: the pair's first / second element lies inside the row (a nest whose
+// pair grid is shifted by one element to align its stores has a half first pair)
+__device__ __forceinline__ double2 dk_ld_A(const double* p, int64_t e, bool lo, bool hi) {
+  if (lo && hi) return *reinterpret_cast<const double2*>(p + e);
+  double2 v; v.x = lo ? p[e] : 0.0; v.y = hi ? p[e + 1] : 0.0; return v;
 }
-__device__ __forceinline__ double2 dk_ld_C(const double* p, int64_t e, bool full) {
-  double2 v; v.x = p[e]; v.y = full ? p[e + 1] : 0.0; return v;
+__device__ __forceinline__ double2 dk_ld_C(const double* p, int64_t e, bool lo, bool hi) {
+  double2 v; v.x = lo ? p[e] : 0.0; v.y = hi ? p[e + 1] : 0.0; return v;
 }
-__device__ __forceinline__ double2 dk_ld_B(const double* p, int64_t, bool) {
+__device__ __forceinline__ double2 dk_ld_B(const double* p, int64_t, bool, bool) {
   double2 v; v.x = p[0]; v.y = v.x; return v;
 }
-__device__ __forceinline__ double2 dk_ld_G(const double* p, int64_t e, bool full, int64_t s) {
-  double2 v; v.x = p[e * s]; v.y = full ? p[(e + 1) * s] : 0.0; return v;
+__device__ __forceinline__ double2 dk_ld_G(const double* p, int64_t e, bool lo, bool hi, int64_t s) {
+  double2 v; v.x = lo ? p[e * s] : 0.0; v.y = hi ? p[(e + 1) * s] : 0.0; return v;
 }
-__device__ __forceinline__ void dk_st_A(double* p, int64_t e, bool full, double x, double y) {
-  if (full) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; }
-  else p[e] = x;
+__device__ __forceinline__ void dk_st_A(double* p, int64_t e, bool lo, bool hi, double x, double y) {
+  if (lo && hi) { double2 v; v.x = x; v.y = y; *reinterpret_cast<double2*>(p + e) = v; return; }
+  if (lo) p[e] = x;
+  if (hi) p[e + 1] = y;
 }
-__device__ __forceinline__ double2 dk_ld_Acs(const double* p, int64_t e, bool full) {
-  if (full) return __ldcs(reinterpret_cast<const double2*>(p + e));
-  double2 v; v.x = __ldcs(p + e); v.y = 0.0; return v;
+__device__ __forceinline__ double2 dk_ld_Acs(const double* p, int64_t e, bool lo, bool hi) {
+  if (lo && hi) return __ldcs(reinterpret_cast<const double2*>(p + e));
+  double2 v; v.x = lo ? __ldcs(p + e) : 0.0; v.y = hi ? __ldcs(p + e + 1) : 0.0; return v;
 }
-__device__ __forceinline__ void dk_st_Acs(double* p, int64_t e, bool full, double x, double y) {
-  if (full) { double2 v; v.x = x; v.y = y; __stcs(reinterpret_cast<double2*>(p + e), v); }
-  else __stcs(p + e, x);
+__device__ __forceinline__ void dk_st_Acs(double* p, int64_t e, bool lo, bool hi, double x, double y) {
+  if (lo && hi) { double2 v; v.x = x; v.y = y; __stcs(reinterpret_cast<double2*>(p + e), v); return; }
+  if (lo) __stcs(p + e, x);
+  if (hi) __stcs(p + e + 1, y);
 }
-__device__ __forceinline__ void dk_st_C(double* p, int64_t e, bool full, double x, double y) {
-  p[e] = x; if (full) p[e + 1] = y;
+__device__ __forceinline__ void dk_st_C(double* p, int64_t e, bool lo, bool hi, double x, double y) {
+  if (lo) p[e] = x;
+  if (hi) p[e + 1] = y;
 }
-__device__ __forceinline__ void dk_st_G(double* p, int64_t e, bool full, double x, double y, int64_t s) {
-  p[e * s] = x; if (full) p[(e + 1) * s] = y;
+__device__ __forceinline__ void dk_st_G(double* p, int64_t e, bool lo, bool hi, double x, double y, int64_t s) {
+  if (lo) p[e * s] = x;
+  if (hi) p[(e + 1) * s] = y;
 }
 
 // ---- K3: TMA tile staging (cp.async.bulk.tensor + mbarrier) ----
@@ -785,7 +811,7 @@ class Gen {
       } else {
         const char c = s.cls;
         o << "        v" << i << "[u] = dk_ld_" << c << "((double*)P.s[" << i << "].p + row * P.s[" << i
-          << "].st[0], e, full";
+          << "].st[0], e, true, full";
         if (c == 'G') o << ", P.s[" << i << "].sti";
         o << ");\n";
       }
@@ -800,7 +826,7 @@ class Gen {
     for (int w : wslots) {
       int si = site_index(np, w, {});
       const char c = np.sites[si].cls;
-      o << "        dk_st_" << c << "((double*)P.s[" << si << "].p + row * P.s[" << si << "].st[0], e, full, w" << w
+      o << "        dk_st_" << c << "((double*)P.s[" << si << "].p + row * P.s[" << si << "].st[0], e, true, full, w" << w
         << "_x, w" << w << "_y";
       if (c == 'G') o << ", P.s[" << si << "].sti";
       o << ");\n";
@@ -846,7 +872,10 @@ class Gen {
     }
 
     for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
-    o << "  const int64_t nrows = P.h.nrows, ninner = P.h.ninner, npairs = (ninner + 1) >> 1;\n";
+    // np.shift = 1: element pairs start one element before the row (e = 2q - 1)
+    // so that the stored views' pairs are 16-byte aligned
+    const int h = np.shift;
+    o << "  const int64_t nrows = P.h.nrows, ninner = P.h.ninner, npairs = (ninner + " << 1 + h << ") >> 1;\n";
     o << "  const int TX = blockDim.x;\n";
     o << "  for (int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; row < nrows; row += (int64_t)gridDim.y * blockDim.y) {\n";
     // outer indices of this row
@@ -864,39 +893,72 @@ class Gen {
       for (int d = 0; d < r - 1; ++d) o << " + oi[" << d << "] * P.s[" << i << "].st[" << d << "]";
       o << ";\n";
     }
-    o << "    for (int64_t q0 = (int64_t)blockIdx.x * TX * " << kUnroll << " + threadIdx.x; q0 < npairs; q0 += (int64_t)gridDim.x * TX * " << kUnroll << ") {\n";
+    // 'H' sites (odd element parity against the pair grid) move as aligned
+    // 16-byte pairs shifted by one element, completed across lanes with a warp
+    // shuffle: warps lie along the row (TX is a multiple of 32) and stay
+    // converged through the pair loop (the loop bound is per warp)
+    bool anyH = false;
+    for (const Site& st : np.sites) anyH |= st.cls == 'H';
+    o << "    const int lane = threadIdx.x & 31; (void)lane;\n";
+    o << "    for (int64_t q0 = (int64_t)blockIdx.x * TX * " << kUnroll << " + threadIdx.x; q0" << (anyH ? " - lane" : "")
+      << " < npairs; q0 += (int64_t)gridDim.x * TX * " << kUnroll << ") {\n";
+    const std::string qline = "        const int64_t q = q0 + (int64_t)u * TX; const bool act = q < npairs;\n"
+            "        const int64_t e = 2 * q - " + std::to_string(h) + "; const bool lo = " +
+            (h ? "e >= 0" : "true") + ", hi = e + 1 < ninner;\n";
     // phase 1: loads
     for (int i = 0; i < NS; ++i) {
       if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
       o << "      double2 v" << i << "[" << kUnroll << "];\n";
     }
-    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n";
-    o << "        const int64_t q = q0 + (int64_t)u * TX;\n";
-    o << "        if (q < npairs) {\n          const int64_t e = 2 * q; const bool full = e + 1 < ninner;\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n" << qline;
+    o << "        if (act) {\n";
     for (int i = 0; i < NS; ++i) {
-      if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
+      if (np.sites[i].cls == 'S' || np.sites[i].cls == 'H' || !np.site_loaded[i]) continue;
       const char c = np.sites[i].cls;
-      o << "          v" << i << "[u] = dk_ld_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << i << ", e, full";
+      o << "          v" << i << "[u] = dk_ld_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << i << ", e, lo, hi";
       if (c == 'G') o << ", P.s[" << i << "].sti";
       o << ");\n";
     }
-    o << "        }\n      }\n";
+    o << "        }\n";
+    for (int i = 0; i < NS; ++i) {
+      if (np.sites[i].cls != 'H' || !np.site_loaded[i]) continue;
+      // lane L loads elements (e+1, e+2); its e comes from lane L-1, lane 0 reads it alone
+      o << "        { double2 a = make_double2(0.0, 0.0);\n"
+        << "          if (act && hi) { if (e + 2 < ninner) a = *reinterpret_cast<const double2*>(b" << i
+        << " + e + 1); else a.x = b" << i << "[e + 1]; }\n"
+        << "          double x = __shfl_up_sync(0xffffffffu, a.y, 1);\n"
+        << "          if (lane == 0 && act && lo) x = b" << i << "[e];\n"
+        << "          v" << i << "[u].x = x; v" << i << "[u].y = a.x; }\n";
+    }
+    o << "      }\n";
     // phase 2: compute + store
-    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n";
-    o << "        const int64_t q = q0 + (int64_t)u * TX;\n";
-    o << "        if (q < npairs) {\n        const int64_t e = 2 * q; const bool full = e + 1 < ninner;\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n" << qline;
     for (int w : wslots) o << "        double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
-    o << "        {\n" << lane_code(np, ne, "x") << "        }\n";
-    o << "        if (full) {\n" << lane_code(np, ne, "y") << "        }\n";
+    o << "        if (act) {\n";
+    o << "        if (lo) {\n" << lane_code(np, ne, "x") << "        }\n";
+    o << "        if (hi) {\n" << lane_code(np, ne, "y") << "        }\n";
     for (int w : wslots) {
       int si = site_index(np, w, {});
       const char c = np.sites[si].cls;
-      o << "        dk_st_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << si << ", e, full, w" << w << "_x, w" << w
+      if (c == 'H') continue;
+      o << "        dk_st_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << si << ", e, lo, hi, w" << w << "_x, w" << w
         << "_y";
       if (c == 'G') o << ", P.s[" << si << "].sti";
       o << ");\n";
     }
-    o << "        }\n      }\n";
+    o << "        }\n";
+    for (int w : wslots) {
+      int si = site_index(np, w, {});
+      if (np.sites[si].cls != 'H') continue;
+      // lane L stores elements (e+1, e+2) = (its y, lane L+1's x); lane 0 stores its x alone
+      o << "        { const double nx = __shfl_down_sync(0xffffffffu, w" << w << "_x, 1);\n"
+        << "          if (act) {\n"
+        << "            if (lane == 0 && lo) b" << si << "[e] = w" << w << "_x;\n"
+        << "            if (hi) { if (lane < 31 && q + 1 < npairs) { double2 t; t.x = w" << w << "_y; t.y = nx; "
+        << "*reinterpret_cast<double2*>(b" << si << " + e + 1) = t; } else b" << si << "[e + 1] = w" << w << "_y; }\n"
+        << "          } }\n";
+    }
+    o << "      }\n";
     o << "    }\n  }\n";
     if (NR) emit_reduce_epilogue(o, np, ne, wslots);
     o << "}\n";
@@ -1292,7 +1354,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       o.p = v.ptr + 8ull * (uint64_t)shift;
       for (int d = 0; d < 3 && d + 1 < r; ++d) o.st[d] = str[d];
       o.sti = r ? str[r - 1] : 0;
-      o.mode = s.cls == 'A' ? 0 : s.cls == 'C' ? 1 : s.cls == 'G' ? 3 : 2;  // informational: code is specialised
+      o.mode = s.cls == 'A' ? 0 : s.cls == 'C' || s.cls == 'H' ? 1 : s.cls == 'G' ? 3 : 2;  // informational: code is specialised
     }
     std::vector<dk_view> rd(std::max(NR, 1));
     memset(rd.data(), 0, sizeof(dk_view) * rd.size());
@@ -1326,7 +1388,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     // launch shape
     unsigned gx = 1, gy = 1, tx = kTPB, ty = 1;
     if (r > 0 && h.nelem > 0) {
-      const int64_t npairs = (h.ninner + 1) / 2;
+      const int64_t npairs = (h.ninner + 1 + np.shift) / 2;
       tx = (unsigned)(npairs >= kTPB ? kTPB : std::max<int64_t>(32, pow2ceil(npairs)));
       ty = kTPB / tx;
       const int64_t maxg = (int64_t)S.sm_count * m->occ[n];

@@ -116,3 +116,28 @@ def test_offset_out_of_bounds_detected(rt):
     task = TaskDesc("SHIFT", (2,), (ArgDesc(0, tile, "R"), ArgDesc(1, tile, "W")))
     with pytest.raises(BoundsError):
         codegen(rt, kp, views_for(rt, task, kp, {0: (8,), 1: (8,)}), compile_=False)
+
+
+def test_odd_parity_pair_variants(rt, monkeypatch):
+    """Stencil COPY work -> grid interior (the interior view starts one element
+    past a 16-byte boundary).  Default: aligned 16-byte loads, split 8-byte
+    stores.  DK_JIT_H: the target moves as aligned pairs shifted by one
+    element, completed by a warp shuffle ('H')."""
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    case = {c["name"]: c for c in load_golden("bench_small.json.gz")}["stencil/fused"]
+    tr = PlanTrace.from_json(case["trace"])
+    copy = [e for e in tr.execs() if e.f == 1][0]
+    win = [e for e in tr.execs() if e.f == 5][0]
+
+    def body(e):
+        src = codegen(rt, e.kernel, views_for(rt, e.task, e.kernel, tr.shapes), scalars=e.task.scalars)
+        return src[src.index("__global__"):]
+
+    b = body(copy)
+    assert "q0 < npairs" in b and "dk_ld_A(" in b and "dk_st_C(" in b and "__shfl" not in b
+    monkeypatch.setenv("DK_JIT_H", "1")
+    b = body(copy)
+    assert "q0 - lane < npairs" in b and "__shfl_down_sync" in b and "dk_st_C(" not in b and "dk_ld_C(" not in b
+    b = body(win)  # the window's shifted views (not TMA-staged at this size)
+    assert "__shfl_up_sync" in b and "dk_ld_C(" not in b

@@ -52,6 +52,12 @@ def capture(name, gen, iters, fused, execute=False):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--medium-only" not in sys.argv:
+        full_size()
+    medium()
+
+
+def full_size():
     for N in (1, 2, 4, 8):
         for wl, gen in gens(N).items():
             iters = ITERS + (4 if wl == "bs" else 0)
@@ -77,6 +83,9 @@ def main():
             name = f"{wl}_{'fused' if fused else 'unfused'}_cpu"
             tr = capture(name, gen, 12, fused)
             tr.save(os.path.join(OUT, name + ".json.gz"))
+
+
+def medium():
     # medium sizes for GPU-vs-oracle parity tests (traces only; the oracle runs on the box)
     med = []
     for name, gen in [
@@ -84,6 +93,11 @@ def main():
         ("bs_1e5_k2", lambda: W.blackscholes(100_000, 2, 6)),
         ("stencil_n256_k1", lambda: W.stencil_bands(256, 1, 3)),
         ("stencil_n255_k2", lambda: W.stencil_bands(255, 2, 3)),
+        # row widths around the warp / CTA / pair boundaries of the JIT's row loop
+        ("stencil_n34_k1", lambda: W.stencil_bands(34, 1, 2)),
+        ("stencil_n67_k1", lambda: W.stencil_bands(67, 1, 2)),
+        ("stencil_n1030_k1", lambda: W.stencil_bands(1030, 1, 2)),
+        ("stencil_n1027_k3", lambda: W.stencil_bands(1027, 3, 2)),
         ("cg_64x64_k1", lambda: W.cg_csr(64, 64, 1, 8)),
         ("cg_64x64_k2", lambda: W.cg_csr(64, 64, 2, 8)),
         ("pcg_64x64_k2", lambda: W.pcg_csr(64, 64, 2, 8)),
