@@ -253,9 +253,20 @@ static int kStages() {
   return s;
 }
 
+// grid of a reducing nest: red_waves() x (SMs x resident CTAs) CTAs, one
+// partial per CTA (DK_JIT_RWAVES)
+static int red_waves() {
+  static int w = [] {
+    const char* e = getenv("DK_JIT_RWAVES");
+    return std::min(64, std::max(1, e ? atoi(e) : 4));  // CG windows: 4-8 best, 1 = +2 %
+  }();
+  return w;
+}
+
 struct NestPlan {
   int rank = 0;  // actual domain rank
   int shift = 0;  // 1: element pairs start at column -1 (aligns the odd-parity views)
+  bool oneshot = false;  // one CTA per chunk of pairs (no persistent grid-stride loop)
   bool staged = false;
   int st_rows = 0;         // box rows = kTR + max dr
   int st_sh = 0;           // column shift that 16-byte aligns the tensor base
@@ -493,7 +504,8 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
       for (Site& st : np.sites)
         if (st.cls == 'A' || st.cls == 'C') st.cls = st.par < 0 ? 'C' : st.par == np.shift ? 'A' : useH ? 'H' : 'C';
     }
-    ks << "n" << n << ":r" << r << ":h" << np.shift << ":";
+    np.oneshot = !np.staged && r > 0 && !getenv("DK_JIT_PERSIST");
+    ks << "n" << n << ":r" << r << ":h" << np.shift << (np.oneshot ? "o" : "") << ":";
     if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
@@ -658,14 +670,20 @@ static GenOpts default_opts(const std::vector<NestPlan>& plans) {
     most = std::max(most, n);
     staged |= np.staged;
   }
-  o.unroll = most <= 3 ? 2 : 1;
-  // few-operand streaming nests (elementwise chains, CG vector windows) run
-  // best with 6 resident CTAs (48 warps, <= 40 registers): measured 3.74 ms
-  // vs 3.99 ms at 4 CTAs for the 1e9-option chain (98.7 % of copy bandwidth)
-  // Same-box sweeps: the TMA-staged stencil window runs best at 3 CTAs; nests with an
-  // unaligned (odd-offset) operand at 4 (stencil COPY 3.21 ms vs 3.71 at 6); fully
-  // aligned few-operand nests at 6 (BS 3.94 vs 3.98 ms at 4).
-  o.min_blocks = staged ? 3 : (most <= 3 && all_aligned ? 6 : 4);
+  const bool persist = getenv("DK_JIT_PERSIST") != nullptr;
+  if (persist) {
+    // persistent grid-stride CTAs (the round-1 default): same-box sweeps gave
+    // 3 CTAs/SM for the TMA-staged stencil window, 4 for nests with an
+    // odd-offset operand, 6 for fully aligned few-operand nests
+    o.unroll = most <= 3 ? 2 : 1;
+    o.min_blocks = staged ? 3 : (most <= 3 && all_aligned ? 6 : 4);
+  } else {
+    // one CTA per chunk (see NestPlan::oneshot).  Same-box sweeps (U x CTAs/SM):
+    // BS window (2 operands) 3.40 ms at U=4 vs 3.45 at U=2 and 4.33 at U=8;
+    // stencil COPY 2.47 ms at 6 CTAs/SM vs 2.71 at 4; the staged window keeps 3
+    o.unroll = most <= 2 ? 4 : (most <= 3 ? 2 : 1);
+    o.min_blocks = staged ? 3 : 6;
+  }
   if (const char* u = getenv("DK_JIT_UNROLL")) o.unroll = std::max(1, atoi(u));
   if (const char* m = getenv("DK_JIT_MINB")) o.min_blocks = std::max(1, atoi(m));
   if (const char* c = getenv("DK_JIT_CS")) o.stream_hint = atoi(c) != 0;
@@ -877,7 +895,18 @@ class Gen {
     const int h = np.shift;
     o << "  const int64_t nrows = P.h.nrows, ninner = P.h.ninner, npairs = (ninner + " << 1 + h << ") >> 1;\n";
     o << "  const int TX = blockDim.x;\n";
-    o << "  for (int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; row < nrows; row += (int64_t)gridDim.y * blockDim.y) {\n";
+    if (np.oneshot) {
+      // one chunk of TX x unroll pairs (of blockDim.y rows) per CTA, grid = all
+      // chunks: measured 2.48 ms vs 3.24 ms for a persistent grid-stride walk
+      // over the stencil COPY's 32766 x 32766 interior (tools/gpu/copybench.cu)
+      o << "  const int64_t cpr = (npairs + TX * " << kUnroll << " - 1) / (TX * " << kUnroll
+        << "), nchunks = (nrows + blockDim.y - 1) / blockDim.y * cpr;\n";
+      o << "  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {\n";
+      o << "    const int64_t rg = c / cpr, row = rg * blockDim.y + threadIdx.y;\n";
+      o << "    if (row >= nrows) continue;\n";
+    } else {
+      o << "  for (int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y; row < nrows; row += (int64_t)gridDim.y * blockDim.y) {\n";
+    }
     // outer indices of this row
     if (r == 2) {
       o << "    const int64_t oi[1] = {row};\n";
@@ -900,37 +929,48 @@ class Gen {
     bool anyH = false;
     for (const Site& st : np.sites) anyH |= st.cls == 'H';
     o << "    const int lane = threadIdx.x & 31; (void)lane;\n";
-    o << "    for (int64_t q0 = (int64_t)blockIdx.x * TX * " << kUnroll << " + threadIdx.x; q0" << (anyH ? " - lane" : "")
-      << " < npairs; q0 += (int64_t)gridDim.x * TX * " << kUnroll << ") {\n";
-    const std::string qline = "        const int64_t q = q0 + (int64_t)u * TX; const bool act = q < npairs;\n"
-            "        const int64_t e = 2 * q - " + std::to_string(h) + "; const bool lo = " +
-            (h ? "e >= 0" : "true") + ", hi = e + 1 < ninner;\n";
+    auto qline_of = [&](const std::string& qb) {
+      return "        const int64_t q = " + qb + " + (int64_t)u * TX; const bool act = q < npairs;\n"
+             "        const int64_t e = 2 * q - " + std::to_string(h) + "; const bool lo = " +
+             (h ? "e >= 0" : "true") + ", hi = e + 1 < ninner;\n";
+    };
+    const std::string qline = qline_of("q0");
+    auto emit_loads = [&](const std::string& qb, const std::string& arr, const std::string& ind) {
+      o << ind << "#pragma unroll\n" << ind << "for (int u = 0; u < " << kUnroll << "; ++u) {\n" << qline_of(qb);
+      o << "        if (act) {\n";
+      for (int i = 0; i < NS; ++i) {
+        if (np.sites[i].cls == 'S' || np.sites[i].cls == 'H' || !np.site_loaded[i]) continue;
+        const char c = np.sites[i].cls;
+        o << "          " << arr << i << "[u] = dk_ld_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << i << ", e, lo, hi";
+        if (c == 'G') o << ", P.s[" << i << "].sti";
+        o << ");\n";
+      }
+      o << "        }\n";
+      for (int i = 0; i < NS; ++i) {
+        if (np.sites[i].cls != 'H' || !np.site_loaded[i]) continue;
+        // lane L loads elements (e+1, e+2); its e comes from lane L-1, lane 0 reads it alone
+        o << "        { double2 a = make_double2(0.0, 0.0);\n"
+          << "          if (act && hi) { if (e + 2 < ninner) a = *reinterpret_cast<const double2*>(b" << i
+          << " + e + 1); else a.x = b" << i << "[e + 1]; }\n"
+          << "          double x = __shfl_up_sync(0xffffffffu, a.y, 1);\n"
+          << "          if (lane == 0 && act && lo) x = b" << i << "[e];\n"
+          << "          " << arr << i << "[u].x = x; " << arr << i << "[u].y = a.x; }\n";
+      }
+      o << ind << "}\n";
+    };
+    auto declare = [&](const std::string& arr, const std::string& ind) {
+      for (int i = 0; i < NS; ++i)
+        if (np.sites[i].cls != 'S' && np.site_loaded[i]) o << ind << "double2 " << arr << i << "[" << kUnroll << "];\n";
+    };
+    if (np.oneshot) {
+      o << "    {\n      const int64_t q0 = (c - rg * cpr) * TX * " << kUnroll << " + threadIdx.x;\n";
+    } else {
+      o << "    for (int64_t q0 = (int64_t)blockIdx.x * TX * " << kUnroll << " + threadIdx.x; q0" << (anyH ? " - lane" : "")
+        << " < npairs; q0 += (int64_t)gridDim.x * TX * " << kUnroll << ") {\n";
+    }
     // phase 1: loads
-    for (int i = 0; i < NS; ++i) {
-      if (np.sites[i].cls == 'S' || !np.site_loaded[i]) continue;
-      o << "      double2 v" << i << "[" << kUnroll << "];\n";
-    }
-    o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n" << qline;
-    o << "        if (act) {\n";
-    for (int i = 0; i < NS; ++i) {
-      if (np.sites[i].cls == 'S' || np.sites[i].cls == 'H' || !np.site_loaded[i]) continue;
-      const char c = np.sites[i].cls;
-      o << "          v" << i << "[u] = dk_ld_" << c << (c == 'A' && cs_ ? "cs" : "") << "(b" << i << ", e, lo, hi";
-      if (c == 'G') o << ", P.s[" << i << "].sti";
-      o << ");\n";
-    }
-    o << "        }\n";
-    for (int i = 0; i < NS; ++i) {
-      if (np.sites[i].cls != 'H' || !np.site_loaded[i]) continue;
-      // lane L loads elements (e+1, e+2); its e comes from lane L-1, lane 0 reads it alone
-      o << "        { double2 a = make_double2(0.0, 0.0);\n"
-        << "          if (act && hi) { if (e + 2 < ninner) a = *reinterpret_cast<const double2*>(b" << i
-        << " + e + 1); else a.x = b" << i << "[e + 1]; }\n"
-        << "          double x = __shfl_up_sync(0xffffffffu, a.y, 1);\n"
-        << "          if (lane == 0 && act && lo) x = b" << i << "[e];\n"
-        << "          v" << i << "[u].x = x; v" << i << "[u].y = a.x; }\n";
-    }
-    o << "      }\n";
+    declare("v", "      ");
+    emit_loads("q0", "v", "      ");
     // phase 2: compute + store
     o << "      #pragma unroll\n      for (int u = 0; u < " << kUnroll << "; ++u) {\n" << qline;
     for (int w : wslots) o << "        double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
@@ -1078,8 +1118,12 @@ class Gen {
     o << "  if (!dk_last) return;\n  __threadfence();\n";
     o << "  double dk_tot[" << NA << "];\n";
     for (int a = 0; a < np.n_array_red; ++a) {
-      o << "  { double s = 0.0;\n    #pragma unroll 1\n    for (int64_t i = lin; i < G; i += 256) s = dk_add(s, dk_ldcg(red_part + " << a
-        << " * G + i)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0) dk_sred[" << a << "][wid] = s; }\n";
+      // four independent accumulators keep four partial loads in flight per thread
+      o << "  { const double* rp = red_part + " << a << " * G; double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0; int64_t i = lin;\n"
+        << "    #pragma unroll 1\n    for (; i + 768 < G; i += 1024) { s0 = dk_add(s0, dk_ldcg(rp + i)); s1 = dk_add(s1, dk_ldcg(rp + i + 256));"
+        << " s2 = dk_add(s2, dk_ldcg(rp + i + 512)); s3 = dk_add(s3, dk_ldcg(rp + i + 768)); }\n"
+        << "    #pragma unroll 1\n    for (; i < G; i += 256) s0 = dk_add(s0, dk_ldcg(rp + i));\n"
+        << "    double s = dk_add(dk_add(s0, s1), dk_add(s2, s3)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0) dk_sred[" << a << "][wid] = s; }\n";
     }
     o << "  __syncthreads();\n";
     for (int a = 0; a < np.n_array_red; ++a)
@@ -1261,7 +1305,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     unsigned int* tk = nullptr;
     const int na = std::max(plans[n].n_array_red, 1);
     if (!plans[n].red_slots.empty()) {
-      DK_CUDA(cudaMalloc(&rp, sizeof(double) * (size_t)na * (size_t)sms * occ + 64));
+      DK_CUDA(cudaMalloc(&rp, sizeof(double) * (size_t)na * (size_t)sms * occ * red_waves() + 64));
       DK_CUDA(cudaMalloc(&tk, sizeof(unsigned int) * 4));
       DK_CUDA(cudaMemset(tk, 0, sizeof(unsigned int) * 4));
     }
@@ -1393,12 +1437,20 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       ty = kTPB / tx;
       const int64_t maxg = (int64_t)S.sm_count * m->occ[n];
       const int64_t U = m->unroll;
-      int64_t GX = std::min<int64_t>((npairs + (int64_t)tx * U - 1) / ((int64_t)tx * U), maxg);
-      GX = std::max<int64_t>(GX, 1);
-      int64_t GY = std::min<int64_t>((h.nrows + ty - 1) / ty, std::max<int64_t>(1, maxg / GX));
-      GY = std::min<int64_t>(std::max<int64_t>(GY, 1), 65535);
-      gx = (unsigned)GX;
-      gy = (unsigned)GY;
+      if (np.oneshot) {
+        // reductions keep a bounded grid (one partial per CTA, folded by the last CTA)
+        const int64_t cpr = (npairs + (int64_t)tx * U - 1) / ((int64_t)tx * U);
+        const int64_t cap = np.red_slots.empty() ? 0x7fffffff : red_waves() * maxg;
+        gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((h.nrows + ty - 1) / ty * cpr, cap));
+        gy = 1;
+      } else {
+        int64_t GX = std::min<int64_t>((npairs + (int64_t)tx * U - 1) / ((int64_t)tx * U), maxg);
+        GX = std::max<int64_t>(GX, 1);
+        int64_t GY = std::min<int64_t>((h.nrows + ty - 1) / ty, std::max<int64_t>(1, maxg / GX));
+        GY = std::min<int64_t>(std::max<int64_t>(GY, 1), 65535);
+        gx = (unsigned)GX;
+        gy = (unsigned)GY;
+      }
     } else if (r == 0) {
       tx = 32;
       ty = 1;

@@ -178,7 +178,13 @@ void launch_builtin(const std::string& kind, const dk_view* v, int n, const int3
     if (view_volume(rp) != nrows + 1 && !(nrows == 0 && view_volume(rp) <= 1))
       fail(DK_ERR_ARG, "SPMV_CSR: rowptr has %lld entries for %lld rows", (long long)view_volume(rp), (long long)nrows);
     if (nrows == 0) return;
-    int blocks = (int)std::min<int64_t>((nrows + 255) / 256, (int64_t)sms * 8);
+    // one CTA per 256 rows (no persistent grid-stride loop): as for the JIT's
+    // streaming nests, a grid covering the whole matrix keeps the HBM stream
+    // tighter (0.862 vs 0.875 ms at 67M rows; DK_SPMV_PERSIST restores the
+    // persistent grid).  Staging each CTA's nonzeros in shared memory first
+    // was measured slower (1.17 ms).
+    static const bool persist = getenv("DK_SPMV_PERSIST") != nullptr;
+    const int blocks = (int)std::min<int64_t>((nrows + 255) / 256, persist ? (int64_t)sms * 8 : 0x7fffffff);
     if (rp.dtype == DK_I32)
       k_spmv_csr<int32_t><<<blocks, 256, 0, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
                                                   (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr, nrows);

@@ -120,8 +120,9 @@ def test_offset_out_of_bounds_detected(rt):
 
 def test_odd_parity_pair_variants(rt, monkeypatch):
     """Stencil COPY work -> grid interior (the interior view starts one element
-    past a 16-byte boundary).  Default: aligned 16-byte loads, split 8-byte
-    stores.  DK_JIT_H: the target moves as aligned pairs shifted by one
+    past a 16-byte boundary).  Default: one CTA per chunk of pairs (no
+    persistent grid-stride loop), aligned 16-byte loads, split 8-byte stores.
+    DK_JIT_H: the target moves as aligned pairs shifted by one
     element, completed by a warp shuffle ('H')."""
     from paper_2406_18109_b200.plan import PlanTrace
 
@@ -135,9 +136,9 @@ def test_odd_parity_pair_variants(rt, monkeypatch):
         return src[src.index("__global__"):]
 
     b = body(copy)
-    assert "q0 < npairs" in b and "dk_ld_A(" in b and "dk_st_C(" in b and "__shfl" not in b
+    assert "c < nchunks" in b and "dk_ld_A(" in b and "dk_st_C(" in b and "__shfl" not in b
     monkeypatch.setenv("DK_JIT_H", "1")
     b = body(copy)
-    assert "q0 - lane < npairs" in b and "__shfl_down_sync" in b and "dk_st_C(" not in b and "dk_ld_C(" not in b
+    assert "__shfl_down_sync" in b and "dk_st_C(" not in b and "dk_ld_C(" not in b
     b = body(win)  # the window's shifted views (not TMA-staged at this size)
     assert "__shfl_up_sync" in b and "dk_ld_C(" not in b

@@ -117,11 +117,11 @@ print("checked", n)
 """
 
 
-@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT"])
+@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT", "DK_JIT_PERSIST"])
 def test_stencil_codegen_variants_match_oracle(variant, tmp_path):
     """The stencil plans with the TMA-staged window (K3) off, the shuffled
-    odd-offset pairs ('H') on, or the shifted pair grid off: every code path of
-    the pair loop is checked against the oracle (a fresh process per variant:
+    odd-offset pairs ('H') on, the shifted pair grid off, or persistent
+    grid-stride CTAs instead of one CTA per chunk: every code path of the pair loop is checked against the oracle (a fresh process per variant:
     modules are cached per process)."""
     import subprocess
     import sys

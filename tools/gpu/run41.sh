@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+run() { R=$(env $2 timeout 600 python bench.py --workload $1 --steps 20 --warmup 3 --quick 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['per_exec_ms'])"); echo "$1 $2 $R"; }
+for i in 1 2; do for m in tile row persist; do run cg DK_SPMV=$m; done; done
+run pcg X=1
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+DK_SPMV=row timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
