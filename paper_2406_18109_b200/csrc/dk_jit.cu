@@ -22,6 +22,11 @@
 //     folds the partials in a fixed order and performs buf[()] += total in
 //     statement order (kernels.py:765).  A scalar-valued expression adds
 //     value * volume, like np.sum on a 0-d value does not.
+// Grids: a streaming nest launches one CTA per chunk of 256 x unroll element
+// pairs (the hardware CTA scheduler then sweeps HBM in order; persistent
+// grid-stride CTAs drift apart and lose 15-25 %); a reducing nest keeps a
+// bounded grid (one partial per CTA); a TMA-staged nest runs persistent CTAs
+// that take tiles from an atomic queue.
 // Loads hoisted ahead of the pair's stores are legal because the host rejects
 // bindings where a written view overlaps another view of the same store
 // (the fusion constraints already exclude that for fused windows,
@@ -238,8 +243,8 @@ struct Site {
 
 // K3: aliased views of one store (the stencil's shifted interior views) are
 // staged tile by tile in shared memory by TMA and read from there; each
-// CTA owns a persistent loop over TR x TC output tiles with a 2-stage
-// mbarrier pipeline.
+// persistent CTA takes TR x TC output tiles from an atomic queue (in order
+// across the GPU) through an S-stage mbarrier ring.
 static const int kTR = 8;     // output rows per tile
 static const int kTC = 128;   // output columns per tile (64 element pairs)
 static const int kBW = 136;   // TMA box width (tile + column halo + alignment), 1088 B per row
@@ -266,6 +271,7 @@ static int red_waves() {
 struct NestPlan {
   int rank = 0;  // actual domain rank
   int shift = 0;  // 1: element pairs start at column -1 (aligns the odd-parity views)
+  bool st_queue = false;  // K3 tiles handed out by an atomic queue (else cyclic by CTA)
   bool oneshot = false;  // one CTA per chunk of pairs (no persistent grid-stride loop)
   bool staged = false;
   int st_rows = 0;         // box rows = kTR + max dr
@@ -506,7 +512,9 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
     }
     np.oneshot = !np.staged && r > 0 && !getenv("DK_JIT_PERSIST");
     ks << "n" << n << ":r" << r << ":h" << np.shift << (np.oneshot ? "o" : "") << ":";
-    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << ";";
+    // queue: stencil window 2.82 ms vs 3.20 ms with a cyclic tile walk (DK_K3_CYCLIC)
+    np.st_queue = np.staged && getenv("DK_K3_CYCLIC") == nullptr;
+    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? "q" : "") << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
       ks << s.slot << s.cls;
@@ -611,6 +619,9 @@ __device__ __forceinline__ void dk_tma_2d(const void* tmap, uint32_t bar, uint32
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       :: "r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void dk_mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 __device__ __forceinline__ void dk_mbar_wait(uint32_t bar, uint32_t ph) {
   uint32_t ok = 0;
@@ -793,22 +804,46 @@ class Gen {
     auto tcol = [&](const char* t) { return colmaj ? std::string("(") + t + " / ntr)" : std::string("(") + t + " % ntc)"; };
     o << "  if (tid == 0) {\n    for (int s = 0; s < " << S << "; ++s) dk_mbar_init(dk_smem(&dk_bar[s]), 1);\n";
     o << "    dk_fence_mbar_init();\n  }\n  __syncthreads();\n";
-    o << "  int64_t tile = blockIdx.x;\n";
-    // prologue: S-1 tiles in flight
-    o << "  if (tid == 0)\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
-    o << "      const int64_t t = tile + (int64_t)s * gridDim.x;\n      if (t >= ntiles) break;\n";
-    o << "      dk_tma_2d(&P.tm, dk_smem(&dk_bar[s]), dk_smem(&dk_tile[s][0][0]), (int)(" << tcol("t") << " * " << kTC
-      << "), (int)(" << trow("t") << " * " << kTR << "), " << bytes << "u);\n    }\n";
+    const std::string tma_args_pre = "dk_tma_2d(&P.tm, ";
+    auto tma = [&](const std::string& bar, const std::string& dst, const char* t) {
+      return tma_args_pre + bar + ", " + dst + ", (int)(" + tcol(t) + " * " + std::to_string(kTC) + "), (int)(" + trow(t) +
+             " * " + std::to_string(kTR) + "), " + std::to_string(bytes) + "u);";
+    };
     o << "  const int pr = tid & 63, rg = tid >> 6;\n";
-    o << "  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {\n";
-    o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
-    o << "    const int64_t nxt = tile + (int64_t)" << S - 1 << " * gridDim.x;\n";
-    // the stage refilled here was read in iteration it-1 and released by its __syncthreads
-    o << "    if (tid == 0 && nxt < ntiles) {\n      const int ns = (it + " << S - 1 << ") % " << S << ";\n";
-    o << "      dk_fence_proxy_async();\n";
-    o << "      dk_tma_2d(&P.tm, dk_smem(&dk_bar[ns]), dk_smem(&dk_tile[ns][0][0]), (int)(" << tcol("nxt") << " * " << kTC
-      << "), (int)(" << trow("nxt") << " * " << kTR << "), " << bytes << "u);\n    }\n";
-    o << "    dk_mbar_wait(dk_smem(&dk_bar[stg]), ph);\n";
+    if (np.st_queue) {
+      // dynamic tile queue: tiles are handed out in order by an atomic ticket
+      // (red_ticket[2]); the CTA's thread 0 publishes each stage's tile index
+      // before its TMA (or a plain arrive once the queue is empty)
+      o << "  __shared__ long long dk_tid[" << S << "];\n";
+      o << "  unsigned int* const dk_q = (unsigned int*)P.h.red_ticket + 2;\n";
+      o << "  if (tid == 0)\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
+      o << "      const long long t = (long long)atomicAdd(dk_q, 1u); dk_tid[s] = t;\n";
+      o << "      if (t < ntiles) " << tma("dk_smem(&dk_bar[s])", "dk_smem(&dk_tile[s][0][0])", "t")
+        << " else dk_mbar_arrive(dk_smem(&dk_bar[s]));\n    }\n";
+      o << "  for (int it = 0;; ++it) {\n";
+      o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
+      o << "    if (tid == 0) {\n      const int ns = (it + " << S - 1 << ") % " << S << ";\n";
+      o << "      const long long nxt = (long long)atomicAdd(dk_q, 1u); dk_tid[ns] = nxt;\n";
+      o << "      dk_fence_proxy_async();\n";
+      o << "      if (nxt < ntiles) " << tma("dk_smem(&dk_bar[ns])", "dk_smem(&dk_tile[ns][0][0])", "nxt")
+        << " else dk_mbar_arrive(dk_smem(&dk_bar[ns]));\n    }\n";
+      o << "    dk_mbar_wait(dk_smem(&dk_bar[stg]), ph);\n";
+      o << "    const int64_t tile = dk_tid[stg];\n    if (tile >= ntiles) break;\n";
+    } else {
+      o << "  int64_t tile = blockIdx.x;\n";
+      // prologue: S-1 tiles in flight
+      o << "  if (tid == 0)\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
+      o << "      const int64_t t = tile + (int64_t)s * gridDim.x;\n      if (t >= ntiles) break;\n";
+      o << "      " << tma("dk_smem(&dk_bar[s])", "dk_smem(&dk_tile[s][0][0])", "t") << "\n    }\n";
+      o << "  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {\n";
+      o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
+      o << "    const int64_t nxt = tile + (int64_t)" << S - 1 << " * gridDim.x;\n";
+      // the stage refilled here was read in iteration it-1 and released by its __syncthreads
+      o << "    if (tid == 0 && nxt < ntiles) {\n      const int ns = (it + " << S - 1 << ") % " << S << ";\n";
+      o << "      dk_fence_proxy_async();\n";
+      o << "      " << tma("dk_smem(&dk_bar[ns])", "dk_smem(&dk_tile[ns][0][0])", "nxt") << "\n    }\n";
+      o << "    dk_mbar_wait(dk_smem(&dk_bar[stg]), ph);\n";
+    }
     o << "    const int64_t r0 = " << trow("tile") << " * " << kTR << ", c0 = " << tcol("tile") << " * " << kTC << ";\n";
     o << "    const double (*T)[" << kBW << "] = dk_tile[stg];\n";
     for (int i = 0; i < NS; ++i)
@@ -851,6 +886,10 @@ class Gen {
     }
     o << "      }\n    }\n";
     o << "    __syncthreads();\n  }\n";
+    if (np.st_queue) {
+      // the last CTA out resets the queue for the next launch (stream order)
+      o << "  if (tid == 0) {\n    __threadfence();\n    if (atomicAdd(dk_q + 1, 1u) == gridDim.x - 1) { dk_q[0] = 0u; dk_q[1] = 0u; }\n  }\n";
+    }
     if (NR) emit_reduce_epilogue(o, np, ne, wslots);
     o << "}\n";
   }
@@ -1304,7 +1343,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     double* rp = nullptr;
     unsigned int* tk = nullptr;
     const int na = std::max(plans[n].n_array_red, 1);
-    if (!plans[n].red_slots.empty()) {
+    if (!plans[n].red_slots.empty() || plans[n].staged) {
       DK_CUDA(cudaMalloc(&rp, sizeof(double) * (size_t)na * (size_t)sms * occ * red_waves() + 64));
       DK_CUDA(cudaMalloc(&tk, sizeof(unsigned int) * 4));
       DK_CUDA(cudaMemset(tk, 0, sizeof(unsigned int) * 4));
