@@ -145,6 +145,28 @@ int dk_comm_exchange(int n, const int64_t* sids, const int32_t* peers, const int
 int dk_comm_allgather_f64(uint64_t src, uint64_t dst, int64_t count);
 int dk_comm_barrier(void);
 
+/* Peer-memory reduction exchange (replaces dk_comm_allgather_f64 for fused
+ * kernel reductions; no reference counterpart -- the reference combines
+ * per-point arenas in one host heap, executor.py:193-195).  Every rank owns a
+ * small "board" (DK_P2P_SLOTS ring slots of [world][DK_P2P_POINTS][DK_P2P_RED]
+ * doubles plus one flag per (rank, point)); the boards are IPC-mapped on every
+ * rank, so a reducing kernel's last CTA writes its point's per-statement
+ * totals straight into every rank's board over NVLink and raises the matching
+ * flag there -- the compute step and the all-gather are one kernel. */
+#define DK_P2P_SLOTS 4
+#define DK_P2P_POINTS 16
+#define DK_P2P_RED 32
+/* collective (after dk_comm_init): *enabled = 1 iff every rank mapped every peer's board */
+int dk_p2p_init(int* enabled);
+/* dk_launch with totals published to all ranks' boards: ring slot `slot`,
+ * `point` = ordinal of this launch point among the calling rank's points */
+int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+                  int slot, int point);
+/* stream-ordered wait until counts[q] points of every rank q have published
+ * into this rank's slot (flags consumed); *gathered = the slot's totals,
+ * layout [world][DK_P2P_POINTS][nred] as dk_accum's `vals` */
+int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered);
+
 #ifdef __cplusplus
 }
 #endif

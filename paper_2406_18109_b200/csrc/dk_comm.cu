@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 #include "dk_internal.h"
 
@@ -65,6 +66,34 @@ static RectView rect_view(Store& s, const int64_t* lo, const int64_t* hi) {
   return rv;
 }
 
+// Consume the flags of one board slot: thread (q, j) waits until point j of
+// rank q has published (its kernel's last CTA wrote the totals and then the
+// flag with release semantics at system scope), then clears the flag.  A
+// peer that never publishes is a protocol bug: trap after 10 s instead of
+// hanging the GPU.
+struct P2PCounts {
+  int c[kP2PWMax];
+};
+
+__global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world) {
+  const int q = threadIdx.x / DK_P2P_POINTS, j = threadIdx.x % DK_P2P_POINTS;
+  if (q < world && j < counts.c[q]) {
+    unsigned int* f = flags + q * DK_P2P_POINTS + j;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) __trap();
+      __nanosleep(64);
+    }
+    *f = 0u;
+  }
+  __threadfence_system();
+}
+
 }  // namespace dk
 
 using namespace dk;
@@ -101,6 +130,16 @@ int dk_comm_init(int rank, int world, const uint8_t* id128) {
 int dk_comm_destroy(void) {
   return guard([&] {
     if (!st().comm) return;
+    State& S = st();
+    if (S.p2p) {
+      cudaDeviceSynchronize();
+      for (int q = 0; q < S.world; ++q)
+        if (q != S.rank && S.peer_board[q]) cudaIpcCloseMemHandle((void*)S.peer_board[q]);
+      cudaFree(S.board);
+      S.board = nullptr;
+      memset(S.peer_board, 0, sizeof S.peer_board);
+      S.p2p = false;
+    }
     ncclCommDestroy((ncclComm_t)st().comm);
     st().comm = nullptr;
   });
@@ -154,6 +193,89 @@ int dk_comm_allgather_f64(uint64_t src, uint64_t dst, int64_t count) {
   return guard([&] {
     require_init();
     DK_NCCL(ncclAllGather((const void*)src, (void*)dst, (size_t)count, ncclDouble, comm(), st().stream));
+  });
+}
+
+int dk_p2p_init(int* enabled) {
+  return guard([&] {
+    require_init();
+    ncclComm_t c = comm();
+    State& S = st();
+    *enabled = 0;
+    if (S.p2p) {
+      *enabled = 1;
+      return;
+    }
+    cudaStream_t s = S.stream;
+    int ok = S.world <= kP2PWMax && !getenv("DK_NO_P2P");
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof mine);
+    if (ok) ok = cudaMalloc(&S.board, kP2PBoardBytes) == cudaSuccess;
+    if (ok) ok = cudaMemset(S.board, 0, kP2PBoardBytes) == cudaSuccess;
+    if (ok) ok = cudaIpcGetMemHandle(&mine, S.board) == cudaSuccess;
+    cudaGetLastError();
+    // all-gather the IPC handles (and the success bits) over NCCL
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char* dev = nullptr;
+    DK_CUDA(cudaMalloc(&dev, hb * (S.world + 1) + 8));
+    DK_CUDA(cudaMemcpyAsync(dev + hb * S.world, &mine, hb, cudaMemcpyHostToDevice, s));
+    DK_NCCL(ncclAllGather(dev + hb * S.world, dev, hb, ncclUint8, c, s));
+    std::vector<cudaIpcMemHandle_t> all(S.world);
+    DK_CUDA(cudaMemcpyAsync(all.data(), dev, hb * S.world, cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> opened(S.world, 0);
+    for (int q = 0; q < S.world && ok; ++q) {
+      if (q == S.rank) {
+        S.peer_board[q] = (uint64_t)S.board;
+        continue;
+      }
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      S.peer_board[q] = (uint64_t)p;
+      opened[q] = 1;
+    }
+    // every rank must agree before anyone takes the peer-memory path
+    int* flag = (int*)(dev + hb * S.world);
+    DK_CUDA(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+    DK_NCCL(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, c, s));
+    int all_ok = 0;
+    DK_CUDA(cudaMemcpyAsync(&all_ok, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DK_CUDA(cudaStreamSynchronize(s));
+    DK_CUDA(cudaFree(dev));
+    if (!all_ok) {
+      for (int q = 0; q < S.world; ++q)
+        if (opened[q]) cudaIpcCloseMemHandle((void*)S.peer_board[q]);
+      if (S.board) cudaFree(S.board);
+      S.board = nullptr;
+      memset(S.peer_board, 0, sizeof S.peer_board);
+      cudaGetLastError();
+      return;
+    }
+    S.p2p = true;
+    *enabled = 1;
+  });
+}
+
+int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered) {
+  return guard([&] {
+    require_init();
+    State& S = st();
+    if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
+    if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);
+    P2PCounts pc = {};
+    for (int q = 0; q < S.world; ++q) {
+      if (counts[q] < 0 || counts[q] > DK_P2P_POINTS) fail(DK_ERR_ARG, "rank %d publishes %d points", q, counts[q]);
+      pc.c[q] = counts[q];
+    }
+    char* b = (char*)S.board;
+    k_p2p_wait<<<1, kP2PWMax * DK_P2P_POINTS, 0, S.stream>>>((unsigned int*)(b + p2p_flag_off(slot)), pc, S.world);
+    DK_CUDA(cudaGetLastError());
+    S.launches++;
+    *gathered = (uint64_t)(b + p2p_data_off(slot));
   });
 }
 

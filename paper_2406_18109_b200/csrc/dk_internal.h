@@ -94,7 +94,20 @@ struct State {
   // collectives
   void* comm = nullptr;
   int rank = 0, world = 1;
+  // peer-memory reduction boards (dk_p2p_init): own board + every rank's mapping
+  bool p2p = false;
+  void* board = nullptr;
+  uint64_t peer_board[8] = {};
 };
+
+// board layout: [slot][kP2PWMax][DK_P2P_POINTS][DK_P2P_RED] doubles, then
+// [slot][kP2PWMax][DK_P2P_POINTS] u32 flags
+constexpr int kP2PWMax = 8;
+constexpr size_t kP2PSlotBytes = (size_t)kP2PWMax * DK_P2P_POINTS * DK_P2P_RED * 8;
+constexpr size_t kP2PFlagBytes = (size_t)kP2PWMax * DK_P2P_POINTS * 4;
+inline size_t p2p_data_off(int slot) { return (size_t)slot * kP2PSlotBytes; }
+inline size_t p2p_flag_off(int slot) { return DK_P2P_SLOTS * kP2PSlotBytes + (size_t)slot * kP2PFlagBytes; }
+constexpr size_t kP2PBoardBytes = DK_P2P_SLOTS * (kP2PSlotBytes + kP2PFlagBytes);
 
 State& st();
 void require_init();

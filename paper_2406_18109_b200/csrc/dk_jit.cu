@@ -228,7 +228,15 @@ struct DkSite {
   int64_t sti;
   int64_t mode;  // 0 pair-aligned contiguous, 1 contiguous, 2 broadcast, 3 strided
 };
+// peer publish of a point's totals (last reducing nest of a dk_launch_pub launch)
+struct DkPub {
+  uint64_t src;      // this point's totals block (local board)
+  uint64_t dst[8];   // the same block in every rank's board
+  uint64_t flag[8];  // the point's flag in every rank's board
+  int64_t n, nred;   // ranks to publish to (0: no publish), doubles per block
+};
 static_assert(sizeof(DkHdr) == 8 * 11, "DkHdr layout");
+static_assert(sizeof(DkPub) == 8 * 19, "DkPub layout");
 static_assert(sizeof(DkSite) == 48, "DkSite layout");
 static_assert(sizeof(dk_view) == 80, "dk_view layout");
 
@@ -245,7 +253,16 @@ struct Site {
 // staged tile by tile in shared memory by TMA and read from there; each
 // persistent CTA takes TR x TC output tiles from an atomic queue (in order
 // across the GPU) through an S-stage mbarrier ring.
-static const int kTR = 8;     // output rows per tile
+// output rows per tile (DK_K3_TR: 8, 12 or 16; thread t owns rows (t >> 6) + 4u)
+static int k_tr() {
+  static int v = [] {
+    const char* e = getenv("DK_K3_TR");
+    int t = e ? atoi(e) : 8;
+    return t >= 16 ? 16 : t >= 12 ? 12 : 8;
+  }();
+  return v;
+}
+#define kTR (k_tr())
 static const int kTC = 128;   // output columns per tile (64 element pairs)
 static const int kBW = 136;   // TMA box width (tile + column halo + alignment), 1088 B per row
 // TMA ring depth: S-1 boxes in flight per CTA (DK_K3_STAGES, 2..4)
@@ -539,6 +556,7 @@ typedef unsigned int uint32_t;
 struct dk_view { uint64_t ptr; int32_t rank; int32_t dtype; int64_t ext[4]; int64_t stride[4]; };
 struct DkHdr { int64_t ext[4]; int64_t nrows, ninner, nelem; uint64_t red_part, red_ticket, red_totals; int64_t red_mode; };
 struct DkSite { uint64_t p; int64_t st[3]; int64_t sti; int64_t mode; };
+struct DkPub { uint64_t src; uint64_t dst[8]; uint64_t flag[8]; int64_t n, nred; };
 
 __device__ __forceinline__ double dk_add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dk_sub(double a, double b) { return __dsub_rn(a, b); }
@@ -791,7 +809,9 @@ class Gen {
     for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
     // S-stage ring; an even row count per stage keeps every stage on a 128-byte
     // boundary (TMA destination alignment)
-    const int S = kStages();
+    // static shared memory stays within 48 KB: fewer stages for taller boxes
+    int S = kStages();
+    while (S > 2 && S * ((ROWS + 1) / 2 * 2) * kBW * 8 > 48 * 1024) --S;
     o << "  __shared__ __align__(128) double dk_tile[" << S << "][" << (ROWS + 1) / 2 * 2 << "][" << kBW << "];\n";
     o << "  __shared__ __align__(8) unsigned long long dk_bar[" << S << "];\n";
     o << "  const int tid = threadIdx.x;\n";
@@ -847,8 +867,8 @@ class Gen {
     o << "    const int64_t r0 = " << trow("tile") << " * " << kTR << ", c0 = " << tcol("tile") << " * " << kTC << ";\n";
     o << "    const double (*T)[" << kBW << "] = dk_tile[stg];\n";
     for (int i = 0; i < NS; ++i)
-      if (np.sites[i].cls != 'S' && np.site_loaded[i]) o << "    double2 v" << i << "[2];\n";
-    o << "    #pragma unroll\n    for (int u = 0; u < 2; ++u) {\n";
+      if (np.sites[i].cls != 'S' && np.site_loaded[i]) o << "    double2 v" << i << "[" << kTR / 4 << "];\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < " << kTR / 4 << "; ++u) {\n";
     o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
     o << "      if (row < D0 && e < D1) {\n        const bool full = e + 1 < D1;\n";
     for (int i = 0; i < NS; ++i) {
@@ -870,7 +890,7 @@ class Gen {
       }
     }
     o << "      }\n    }\n";
-    o << "    #pragma unroll\n    for (int u = 0; u < 2; ++u) {\n";
+    o << "    #pragma unroll\n    for (int u = 0; u < " << kTR / 4 << "; ++u) {\n";
     o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
     o << "      if (row < D0 && e < D1) {\n        const bool full = e + 1 < D1;\n";
     for (int w : wslots) o << "        double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
@@ -902,7 +922,7 @@ class Gen {
     const int NR = (int)np.red_slots.size();
     o << "\nstruct P" << n << " { ";
     if (np.staged) o << "alignas(64) unsigned char tm[128]; ";
-    o << "DkHdr h; DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
+    o << "DkHdr h; " << (NR ? "DkPub pub; " : "") << "DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_ << "_n" << n
       << "(const __grid_constant__ P" << n << " P) {\n";
@@ -1134,6 +1154,18 @@ class Gen {
         int si = site_index(np, w, {});
         o << "    *(double*)P.s[" << si << "].p = w" << w << "_s;\n";
       }
+    }
+    if (k) {
+      // peer publish (dk_launch_pub): the point's totals block goes straight
+      // into every rank's board over NVLink, then each board's flag is raised
+      // with release semantics at system scope
+      o << "    if (P.pub.n) {\n      const double* src = (const double*)P.pub.src;\n"
+        << "      for (int q = 0; q < (int)P.pub.n; ++q) { double* d = (double*)P.pub.dst[q];"
+        << " for (int k = 0; k < (int)P.pub.nred; ++k) d[k] = src[k]; }\n"
+        << "      __threadfence_system();\n"
+        << "      for (int q = 0; q < (int)P.pub.n; ++q)"
+        << " asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(P.pub.flag[q]), \"r\"(1u) : \"memory\");\n"
+        << "    }\n";
     }
   }
 
@@ -1377,7 +1409,8 @@ static int64_t pow2ceil(int64_t v) {
   return p;
 }
 
-static void launch(KernelObj& k, const dk_view* views, int nviews, const double* scalars, int nscal, uint64_t totals) {
+static void launch(KernelObj& k, const dk_view* views, int nviews, const double* scalars, int nscal, uint64_t totals,
+                   const DkPub* pub = nullptr) {
   const Prog& g = k.prog;
   if (nviews != g.nslots) fail(DK_ERR_ARG, "launch binds %d views, kernel has %d slots", nviews, g.nslots);
   if (nscal != g.nscal) fail(DK_ERR_ARG, "launch passes %d scalars, kernel expects %d", nscal, g.nscal);
@@ -1385,6 +1418,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   std::string sig((const char*)views, sizeof(dk_view) * (size_t)nviews);
   sig.append((const char*)scalars, 8 * (size_t)nscal);
   sig.append((const char*)&totals, sizeof totals);
+  if (pub) sig.append((const char*)pub, sizeof *pub);
   for (size_t i = 0; i < k.recent.size(); ++i) {
     Prepared& pr = k.recent[i];
     if (pr.sig != sig) continue;
@@ -1424,6 +1458,14 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     h.red_totals = totals ? totals + 8ull * kbase : 0;
     h.red_mode = totals ? 1 : 0;
     const int NS = (int)np.sites.size(), NR = (int)np.red_slots.size();
+    DkPub pb = {};
+    if (pub && NR) {
+      // only the kernel's last reducing nest publishes (the whole block)
+      bool last = true;
+      for (size_t n2 = n + 1; n2 < g.nests.size(); ++n2)
+        if (!fresh[n2].red_slots.empty()) last = false;
+      if (last) pb = *pub;
+    }
     std::vector<DkSite> sites(std::max(NS, 1));
     memset(sites.data(), 0, sizeof(DkSite) * sites.size());
     for (int i = 0; i < NS; ++i) {
@@ -1444,7 +1486,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     for (int q = 0; q < NR; ++q) rd[q] = views[np.red_slots[q]];
     const size_t nsc = std::max(g.nscal, 1);
     const size_t tmb = np.staged ? 128 : 0;  // CUtensorMap (64-byte aligned) leads a staged nest's params
-    size_t total = tmb + sizeof(DkHdr) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc;
+    size_t total = tmb + sizeof(DkHdr) + (NR ? sizeof(DkPub) : 0) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc;
     if (np.staged) total = (total + 63) / 64 * 64;
     blob.assign(total + 64, 0);
     char* p = blob.data();
@@ -1463,6 +1505,10 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     }
     memcpy(p, &h, sizeof h);
     p += sizeof h;
+    if (NR) {
+      memcpy(p, &pb, sizeof pb);
+      p += sizeof pb;
+    }
     memcpy(p, sites.data(), sizeof(DkSite) * sites.size());
     p += sizeof(DkSite) * sites.size();
     memcpy(p, rd.data(), sizeof(dk_view) * rd.size());
@@ -1597,6 +1643,30 @@ int dk_launch(int64_t handle, const dk_view* views, int nviews, const double* sc
   return guard([&] {
     require_init();
     launch(kernel_of(handle), views, nviews, scalars, nscalars, totals);
+  });
+}
+
+int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars, int slot,
+                  int point) {
+  return guard([&] {
+    require_init();
+    State& S = st();
+    if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
+    if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);
+    if (point < 0 || point >= DK_P2P_POINTS) fail(DK_ERR_ARG, "point %d exceeds the board's %d points per rank", point, DK_P2P_POINTS);
+    KernelObj& k = kernel_of(handle);
+    const int nred = k.prog.nreduce;
+    if (nred == 0 || nred > DK_P2P_RED) fail(DK_ERR_UNSUPPORTED, "kernel has %d reductions (board holds 1..%d)", nred, DK_P2P_RED);
+    const size_t off = 8ull * (size_t)nred * (size_t)(S.rank * DK_P2P_POINTS + point);
+    DkPub pub = {};
+    pub.n = S.world;
+    pub.nred = nred;
+    pub.src = (uint64_t)S.board + p2p_data_off(slot) + off;
+    for (int q = 0; q < S.world; ++q) {
+      pub.dst[q] = S.peer_board[q] + p2p_data_off(slot) + off;
+      pub.flag[q] = S.peer_board[q] + p2p_flag_off(slot) + 4ull * (size_t)(S.rank * DK_P2P_POINTS + point);
+    }
+    launch(k, views, nviews, scalars, nscalars, pub.src, &pub);
   });
 }
 

@@ -22,7 +22,12 @@ Reductions.  With one rank every reduce statement accumulates directly into
 its target in point order.  With several, each point's per-statement totals are
 all-gathered and every rank folds ``acc = acc + total_p`` in lexicographic
 point order -- the reference's combine order (executor.py:193-195), so the
-replicated target is bit-identical on all ranks.
+replicated target is bit-identical on all ranks.  When every rank could map
+every peer's reduction board (``dk_p2p_init``), the gather is not a separate
+collective: the reducing kernel's last CTA writes its point's totals into all
+ranks' boards over NVLink and raises a flag there (``dk_launch_pub``); the
+fold waits on the flags of its board slot (``dk_p2p_wait``).  Otherwise, and
+for builtins, the totals go through an NCCL all-gather.
 """
 
 from __future__ import annotations
@@ -74,6 +79,7 @@ class LaunchStats:
     bytes_moved: int = 0
     transfers: int = 0
     inits: int = 0
+    p2p_folds: int = 0  # reductions gathered through the peer-memory boards
 
 
 class Executor:
@@ -111,12 +117,24 @@ class Executor:
         self._plans: dict[tuple, tuple] = {}  # launch-plan cache (one GPU)
         self.stats = LaunchStats()
         self._comm = False
+        self._p2p = False
+        self._p2p_epoch = 0
 
     # ------------------------------------------------------------------ comm
     def init_comm(self, unique_id: bytes) -> None:
         buf = (c_uint8 * 128)(*unique_id)
         check(self.lib.dk_comm_init(self.rank, self.world, buf))
         self._comm = True
+        self.enable_p2p()
+
+    def enable_p2p(self) -> bool:
+        """Collective: switch kernel reductions to the peer-memory board exchange
+        if every rank mapped every peer's board (DK_P2P=0 keeps NCCL)."""
+        if self.world > 1 and os.environ.get("DK_P2P", "1") != "0":
+            ok = c_int(0)
+            check(self.lib.dk_p2p_init(byref(ok)))
+            self._p2p = bool(ok.value)
+        return self._p2p
 
     def comm_unique_id(self) -> bytes:
         buf = (c_uint8 * 128)()
@@ -604,18 +622,24 @@ class Executor:
         V = len(prank)
         totals = 0
         maxp = 0
+        pub_slot = -1
         if use_totals:
             counts = [0] * self.world
             for q in prank:
                 counts[q] += 1
             maxp = max(counts)
+            if self._p2p and maxp <= runtime.P2P_POINTS and nred <= runtime.P2P_RED:
+                pub_slot = self._p2p_epoch % runtime.P2P_SLOTS
+                self._p2p_epoch += 1
+                use_totals = False
+        if use_totals:
             nbytes = 8 * maxp * nred
             tb = c_uint64()
             check(self.lib.dk_scratch_alloc(nbytes * (self.world + 1), byref(tb)))
             totals = tb.value
             check(self.lib.dk_memset_zero(totals, nbytes * (self.world + 1)))
         has_local = any(s.local for s in kp.slots)
-        recorded = [] if not (use_totals or has_local) else None
+        recorded = [] if not (use_totals or has_local or pub_slot >= 0) else None
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * nslots)()
             rp = rects[i]
@@ -645,23 +669,31 @@ class Executor:
                     r = self.stores[task.args[s.arg].store]
                     self._ensure(r, rect)
                     views[si] = self.view(r, rect)
-            tot = totals + 8 * nred * (self.rank * maxp + slot_in_rank) if use_totals else 0
-            check(self.lib.dk_launch(h, views, nslots, scal, len(task.scalars), tot))
+            if pub_slot >= 0:
+                check(self.lib.dk_launch_pub(h, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank))
+            else:
+                tot = totals + 8 * nred * (self.rank * maxp + slot_in_rank) if use_totals else 0
+                check(self.lib.dk_launch(h, views, nslots, scal, len(task.scalars), tot))
             for p in scratch:
                 check(self.lib.dk_scratch_free(p))
             if recorded is not None:
                 recorded.append(views)
         if use_totals:
-            self._fold(task, kp, prank, rects, red_targets, totals, maxp, nred)
+            block = maxp * nred
+            gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
+            check(self.lib.dk_comm_allgather_f64(totals + 8 * block * self.rank, gathered, block))
+            self._fold(task, kp, prank, rects, red_targets, gathered, maxp, nred)
             check(self.lib.dk_scratch_free(totals))
+        elif pub_slot >= 0:
+            g = c_uint64()
+            check(self.lib.dk_p2p_wait(pub_slot, (c_int32 * self.world)(*counts), byref(g)))
+            self._fold(task, kp, prank, rects, red_targets, g.value, runtime.P2P_POINTS, nred)
+            self.stats.p2p_folds += 1
         return recorded
 
-    def _fold(self, task, kp, prank, rects, red_targets, totals, maxp, nred) -> None:
-        """All-gather per-point totals; fold in lexicographic point order."""
+    def _fold(self, task, kp, prank, rects, red_targets, gathered, maxp, nred) -> None:
+        """Fold gathered per-point totals ([world][maxp][nred]) in lexicographic point order."""
         V = len(prank)
-        block = maxp * nred
-        gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
-        check(self.lib.dk_comm_allgather_f64(totals + 8 * block * self.rank, gathered, block))
         slot_of_point = []
         seen = [0] * self.world
         for q in prank:

@@ -329,6 +329,46 @@ class FakeLib:
             out[q * count : (q + 1) * count] = parts[q].numpy()
         return 0
 
+    # ---- peer-memory reduction boards: publish = write into the local board;
+    # the wait all-gathers each rank's own rows of the slot (gloo)
+    def dk_p2p_init(self, ref):
+        from paper_2406_18109_b200 import runtime as rt
+
+        self.p2p_slot_doubles = 8 * rt.P2P_POINTS * rt.P2P_RED
+        if getattr(self, "board", None) is None:
+            self.board, self.board_ptr = self._alloc(8 * rt.P2P_SLOTS * self.p2p_slot_doubles)
+        self.p2p_nred = {}
+        _set(ref, 1 if getattr(self, "p2p_enabled", False) else 0)
+        return 0
+
+    def dk_launch_pub(self, h, views, nviews, scalars, nscal, slot, point):
+        from paper_2406_18109_b200 import runtime as rt
+
+        nred = sum(1 for _, _, sts in self.kernels[h].nests for st in sts if st[0] == "reduce")
+        assert 0 <= point < rt.P2P_POINTS and 0 < nred <= rt.P2P_RED
+        off = 8 * (slot * self.p2p_slot_doubles + nred * (self.rank * rt.P2P_POINTS + point))
+        self.p2p_nred[slot] = nred
+        return self.dk_launch(h, views, nviews, scalars, nscal, self.board_ptr + off)
+
+    def dk_p2p_wait(self, slot, counts, ref):
+        import torch
+        import torch.distributed as dist
+
+        from paper_2406_18109_b200 import runtime as rt
+
+        n = self.p2p_slot_doubles
+        mine = self.allocs[self.board][8 * slot * n : 8 * (slot + 1) * n].view(np.float64)
+        t = torch.from_numpy(np.concatenate([mine, [float(self.p2p_nred.pop(slot, 0))]]))
+        parts = [torch.empty(n + 1, dtype=torch.float64) for _ in range(self.world)]
+        dist.all_gather(parts, t)
+        nred = int(max(float(p[-1]) for p in parts))
+        blk = rt.P2P_POINTS * nred
+        for q in range(self.world):
+            if q != self.rank:
+                mine[q * blk : q * blk + counts[q] * nred] = parts[q].numpy()[q * blk : q * blk + counts[q] * nred]
+        _set(ref, self.board_ptr + 8 * slot * n)
+        return 0
+
     def dk_comm_barrier(self):
         import torch.distributed as dist
 

@@ -44,6 +44,7 @@ def gpusession_drop_in(rank, world, local):
                      ("jacobi", dict(size=32, nodes=world, iters=3))]:
         s = GpuSession(SessionConfig(), rank=rank, world=world, device=local)
         s.executor._comm = True  # communicator already initialised in this process
+        s.executor.enable_p2p()
         rep = run_events(s, gen_benchmark(name, **kw))
         got = {sid: s.heap.get(sid) for sid in s.live_store_ids()}
         s.executor.close()
@@ -67,7 +68,7 @@ def main():
     dist.init_process_group("gloo")
     cases = {c["name"]: c for c in load_golden("bench_small.json.gz") + load_golden("fuzz250.json.gz")}
     names = NAMES + [f"fuzz{s}/fused" for s in range(0, 250, 5)]
-    bad, moved, exact, close = [], 0, 0, 0
+    bad, moved, exact, close, p2p_folds = [], 0, 0, 0, 0
     uid = None
     for name in names:
         case = cases[name]
@@ -81,9 +82,11 @@ def main():
             uid = True
         else:
             ex._comm = True
+            ex.enable_p2p()
         replay(ex, tr.events)
         got = {s: ex.get(s) for s in tr.live}
         moved += ex.stats.transfers
+        p2p_folds += ex.stats.p2p_folds
         ex.close()
         if rank == 0:
             for s, w in golden_arrays(case).items():
@@ -95,7 +98,8 @@ def main():
                     bad.append((name, s))
     bad += gpusession_drop_in(rank, world, local)
     if rank == 0:
-        print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved}")
+        print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved} "
+              f"p2p_folds={p2p_folds} (DK_P2P={os.environ.get('DK_P2P', '1')})")
         if bad:
             sys.exit(1)
     dist.barrier()

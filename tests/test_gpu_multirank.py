@@ -20,12 +20,15 @@ def _ngpus():
         return 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_golden_plans_on_n_gpus(world):
+@pytest.mark.parametrize("world,p2p", [(2, "1"), (2, "0"), (4, "1")])
+def test_golden_plans_on_n_gpus(world, p2p):
+    """p2p=1: kernel reductions gathered through the NVLink peer boards; 0: NCCL all-gather."""
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29511", os.path.join(HERE, "mgpu_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=dict(os.environ, DK_P2P=p2p))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MGPU" in r.stdout and "bad=[]" in r.stdout
+    if p2p == "1":
+        assert "p2p_folds=0 " not in r.stdout, r.stdout[-2000:]

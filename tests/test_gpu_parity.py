@@ -117,7 +117,8 @@ print("checked", n)
 """
 
 
-@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT", "DK_JIT_PERSIST", "DK_K3_CYCLIC"])
+@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT", "DK_JIT_PERSIST", "DK_K3_CYCLIC",
+                                     "DK_K3_TR=12", "DK_K3_TR=16"])
 def test_stencil_codegen_variants_match_oracle(variant, tmp_path):
     """The stencil plans with the TMA-staged window (K3) off, the shuffled
     odd-offset pairs ('H') on, the shifted pair grid off, or persistent
@@ -128,7 +129,8 @@ def test_stencil_codegen_variants_match_oracle(variant, tmp_path):
 
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, DK_REPO=repo, DK_JIT_CACHE=str(tmp_path))
-    env[variant] = "1"
+    key, _, val = variant.partition("=")
+    env[key] = val or "1"
     out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], env=env, capture_output=True, text=True,
                          timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, names, q):
+def _worker(rank, world, port, names, q, p2p=False):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -58,10 +58,13 @@ def _worker(rank, world, port, names, q):
         ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, rank=rank,
                       world=world, lib=lib)
         ex._comm = True
+        if p2p:
+            lib.p2p_enabled = True
+            assert ex.enable_p2p()
         try:
             replay(ex, trace.events)
             got = {s: ex.get(s) for s in trace.live}
-            moved += ex.stats.transfers
+            moved += ex.stats.p2p_folds if p2p else ex.stats.transfers
             if rank == 0:
                 want = want_arrays if want_arrays is not None else golden_arrays(case)
                 for s, w in want.items():
@@ -74,11 +77,11 @@ def _worker(rank, world, port, names, q):
     dist.destroy_process_group()
 
 
-def _run(names, world=2):
+def _run(names, world=2, p2p=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]
@@ -108,6 +111,19 @@ def test_benchmarks_two_ranks_match_reference():
     assert not bad, bad[:10]
     # the multi-point stencils and the CSR CG need halos / replicated reads
     assert res[0][2] > 0 and res[1][2] > 0
+
+
+def test_peer_board_reductions_match_reference():
+    """Reductions gathered through the peer-memory boards (dk_launch_pub /
+    dk_p2p_wait; the fake device all-gathers each rank's board rows) instead of
+    the NCCL all-gather: same heaps, on 2 and 3 ranks (uneven point mapping)."""
+    names = ["stencil_bands_n8_k2/fused", "cg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused", "pcg_csr_8x8_k2/fused",
+             "cg_like/fused", "stencil/fused", "edge_empty_tiles/fused", "edge_rank0/fused", "edge_ragged_2d/fused"]
+    for world in (2, 3):
+        res = _run(names, world=world, p2p=True)
+        bad = [b for _, bs, _ in res for b in bs]
+        assert not bad, bad[:10]
+        assert all(folds > 0 for _, _, folds in res), res
 
 
 def test_uneven_point_mapping_three_ranks():
