@@ -235,6 +235,11 @@ struct DkPub {
   uint64_t flag[8];  // the point's flag in every rank's board
   int64_t n, nred;   // ranks to publish to (0: no publish), doubles per block
 };
+// union region of a register-swept K3 nest
+struct DkUni {
+  uint64_t base;
+  int64_t rs, cols, rows;
+};
 static_assert(sizeof(DkHdr) == 8 * 11, "DkHdr layout");
 static_assert(sizeof(DkPub) == 8 * 19, "DkPub layout");
 static_assert(sizeof(DkSite) == 48, "DkSite layout");
@@ -275,6 +280,27 @@ static int kStages() {
   return s;
 }
 
+// K3 register sweep (DK_K3S=1, opt-in): instead of TMA tiles, each thread
+// walks a column of element pairs down a block of kSweepRows() rows, keeping
+// the stencil's row window in registers and the next kSweepAhead() rows in
+// flight.  Measured slower than the TMA ring for the 32768^2 stencil window
+// (3.42-3.48 ms vs 3.01 ms on the same box for RB 32..256, PF 2..6, 3..5
+// CTAs/SM), so the TMA path stays the default.
+static int kSweepRows() {
+  static int v = [] {
+    const char* e = getenv("DK_K3S_RB");
+    return std::min(1024, std::max(8, e ? atoi(e) : 64));
+  }();
+  return v;
+}
+static int kSweepAhead() {
+  static int v = [] {
+    const char* e = getenv("DK_K3S_PF");
+    return std::min(8, std::max(1, e ? atoi(e) : 3));
+  }();
+  return v;
+}
+
 // grid of a reducing nest: red_waves() x (SMs x resident CTAs) CTAs, one
 // partial per CTA (DK_JIT_RWAVES)
 static int red_waves() {
@@ -302,6 +328,9 @@ struct NestPlan {
   std::vector<int> red_slots;      // target slot per reduce statement (statement order)
   std::vector<char> red_is_array;  // per reduce statement
   int n_array_red = 0;
+  bool sweep = false;  // K3 as a register sweep (no TMA): see nest_sweep
+  int sw_np = 1;       // union element pairs per row per thread
+  int st_maxdr = 0;
 };
 
 static bool nonzero(const std::vector<int64_t>& o) {
@@ -386,6 +415,7 @@ static void plan_staging(NestPlan& np, const dk_view* views, const int64_t* D, i
   if (D[1] + (max_dc - min_dc) + sh > rs) return;  // the union must not wrap across rows
   np.staged = true;
   np.st_rows = kTR + max_dr;
+  np.st_maxdr = max_dr;
   np.st_sh = sh;
   np.st_anchor = anchor_i;
   np.st_min_dc = min_dc;
@@ -511,6 +541,15 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
       if (r == 0 && s.cls != 'S') fail(DK_ERR_UNSUPPORTED, "rank-0 nest over an array operand");
     }
     plan_staging(np, views, D, r, kstored);
+    if (np.staged && getenv("DK_K3S")) {
+      int maxcol = 0;
+      for (const Site& st : np.sites)
+        if (st.staged) maxcol = std::max(maxcol, st.dc - np.st_min_dc + np.st_sh);
+      if (maxcol <= 4) {
+        np.sweep = true;
+        np.sw_np = (maxcol + 1) / 2 + 1;
+      }
+    }
     if (!np.staged && r > 0 && !getenv("DK_JIT_NO_SHIFT")) {
       // pick the pair grid (start column 0 or -1) that 16-byte aligns the most
       // operands; the others move as shuffled pairs ('H')
@@ -531,7 +570,9 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
     ks << "n" << n << ":r" << r << ":h" << np.shift << (np.oneshot ? "o" : "") << ":";
     // queue: stencil window 2.82 ms vs 3.20 ms with a cyclic tile walk (DK_K3_CYCLIC)
     np.st_queue = np.staged && getenv("DK_K3_CYCLIC") == nullptr;
+    if (np.sweep) np.st_queue = false;
     if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? "q" : "") << ";";
+    if (np.sweep) ks << "K3S:" << np.sw_np << "," << kSweepRows() << "," << kSweepAhead() << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
       ks << s.slot << s.cls;
@@ -557,6 +598,17 @@ struct dk_view { uint64_t ptr; int32_t rank; int32_t dtype; int64_t ext[4]; int6
 struct DkHdr { int64_t ext[4]; int64_t nrows, ninner, nelem; uint64_t red_part, red_ticket, red_totals; int64_t red_mode; };
 struct DkSite { uint64_t p; int64_t st[3]; int64_t sti; int64_t mode; };
 struct DkPub { uint64_t src; uint64_t dst[8]; uint64_t flag[8]; int64_t n, nred; };
+struct DkUni { uint64_t base; int64_t rs, cols, rows; };
+// element pair q of row r of a K3 union region (16-byte aligned base, even row stride)
+__device__ __forceinline__ double2 dk_ldu(const DkUni& u, int64_t r, int64_t q) {
+  double2 v; v.x = 0.0; v.y = 0.0;
+  if (r < u.rows) {
+    const double* p = (const double*)u.base + r * u.rs + 2 * q;
+    if (2 * q + 1 < u.cols) v = __ldg(reinterpret_cast<const double2*>(p));
+    else if (2 * q < u.cols) v.x = __ldg(p);
+  }
+  return v;
+}
 
 __device__ __forceinline__ double dk_add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dk_sub(double a, double b) { return __dsub_rn(a, b); }
@@ -713,6 +765,9 @@ static GenOpts default_opts(const std::vector<NestPlan>& plans) {
     o.unroll = most <= 2 ? 4 : (most <= 3 ? 2 : 1);
     o.min_blocks = staged ? 3 : 6;
   }
+  bool sweep = false;
+  for (const NestPlan& np : plans) sweep |= np.sweep;
+  if (sweep) o.min_blocks = 4;
   if (const char* u = getenv("DK_JIT_UNROLL")) o.unroll = std::max(1, atoi(u));
   if (const char* m = getenv("DK_JIT_MINB")) o.min_blocks = std::max(1, atoi(m));
   if (const char* c = getenv("DK_JIT_CS")) o.stream_hint = atoi(c) != 0;
@@ -914,6 +969,76 @@ class Gen {
     o << "}\n";
   }
 
+  // K3 as a register sweep: thread t of a CTA owns domain element pair
+  // (task column chunk x 256 + t) and walks kSweepRows() rows of it; the
+  // union rows r .. r + max_dr of the aliased views sit in registers (W), the
+  // next kSweepAhead() union rows are already loaded (F), every union row is
+  // read once per chunk with 16-byte aligned loads (the neighbouring pair comes
+  // from L1: the next lane loaded it).  No shared memory, no barriers.
+  void nest_sweep(std::ostringstream& o, int n, const std::vector<int>& wslots) const {
+    const NestIR& ne = g_.nests[n];
+    const NestPlan& np = plans_[n];
+    const int NS = (int)np.sites.size();
+    const int NR = (int)np.red_slots.size();
+    const int NRW = np.st_maxdr + 1, NPR = np.sw_np, PF = kSweepAhead(), RB = kSweepRows();
+    for (int a = 0; a < np.n_array_red; ++a) o << "  double racc" << a << " = 0.0;\n";
+    o << "  const int64_t D0 = P.h.ext[0], D1 = P.h.ext[1];\n";
+    o << "  const int64_t ncc = (((D1 + 1) >> 1) + 255) >> 8, nrb = (D0 + " << RB - 1 << ") / " << RB
+      << ", ntask = ncc * nrb;\n";
+    o << "  for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {\n";
+    o << "    const int u = 0; (void)u;\n";
+    o << "    const int64_t cc = task % ncc, rb = task / ncc, pp = (cc << 8) + threadIdx.x, e = 2 * pp;\n";
+    o << "    if (e >= D1) continue;\n";
+    o << "    const bool full = e + 1 < D1;\n";
+    o << "    const int64_t r0 = rb * " << RB << ", r1 = r0 + " << RB << " < D0 ? r0 + " << RB << " : D0;\n";
+    o << "    double2 W[" << NRW << "][" << NPR << "], F[" << PF << "][" << NPR << "];\n";
+    for (int k = 0; k + 1 < NRW; ++k)
+      for (int c = 0; c < NPR; ++c) o << "    W[" << k << "][" << c << "] = dk_ldu(P.u, r0 + " << k << ", pp + " << c << ");\n";
+    for (int j = 0; j < PF; ++j)
+      for (int c = 0; c < NPR; ++c)
+        o << "    F[" << j << "][" << c << "] = dk_ldu(P.u, r0 + " << NRW - 1 + j << ", pp + " << c << ");\n";
+    o << "    for (int64_t row = r0; row < r1; ++row) {\n";
+    for (int c = 0; c < NPR; ++c) o << "      W[" << NRW - 1 << "][" << c << "] = F[0][" << c << "];\n";
+    for (int j = 0; j + 1 < PF; ++j)
+      for (int c = 0; c < NPR; ++c) o << "      F[" << j << "][" << c << "] = F[" << j + 1 << "][" << c << "];\n";
+    for (int c = 0; c < NPR; ++c)
+      o << "      F[" << PF - 1 << "][" << c << "] = dk_ldu(P.u, row + " << NRW - 1 + PF << ", pp + " << c << ");\n";
+    for (int i = 0; i < NS; ++i) {
+      const Site& st = np.sites[i];
+      if (st.cls == 'S' || !np.site_loaded[i]) continue;
+      o << "      double2 v" << i << "[1];\n";
+      if (st.staged) {
+        const int col = st.dc - np.st_min_dc + np.st_sh, c2 = col / 2;
+        if (col % 2 == 0)
+          o << "      v" << i << "[0] = W[" << st.dr << "][" << c2 << "];\n";
+        else
+          o << "      v" << i << "[0].x = W[" << st.dr << "][" << c2 << "].y; v" << i << "[0].y = W[" << st.dr << "]["
+            << c2 + 1 << "].x;\n";
+      } else {
+        const char c = st.cls;
+        o << "      v" << i << "[0] = dk_ld_" << c << "((double*)P.s[" << i << "].p + row * P.s[" << i << "].st[0], e, true, full";
+        if (c == 'G') o << ", P.s[" << i << "].sti";
+        o << ");\n";
+      }
+    }
+    for (int w : wslots) o << "      double w" << w << "_x = 0.0, w" << w << "_y = 0.0;\n";
+    o << "      {\n" << lane_code(np, ne, "x") << "      }\n";
+    o << "      if (full) {\n" << lane_code(np, ne, "y") << "      }\n";
+    for (int w : wslots) {
+      int si = site_index(np, w, {});
+      const char c = np.sites[si].cls;
+      o << "      dk_st_" << c << "((double*)P.s[" << si << "].p + row * P.s[" << si << "].st[0], e, true, full, w" << w
+        << "_x, w" << w << "_y";
+      if (c == 'G') o << ", P.s[" << si << "].sti";
+      o << ");\n";
+    }
+    for (int k = 0; k + 1 < NRW; ++k)
+      for (int c = 0; c < NPR; ++c) o << "      W[" << k << "][" << c << "] = W[" << k + 1 << "][" << c << "];\n";
+    o << "    }\n  }\n";
+    if (NR) emit_reduce_epilogue(o, np, ne, wslots);
+    o << "}\n";
+  }
+
   void nest(std::ostringstream& o, int n) const {
     const NestIR& ne = g_.nests[n];
     const NestPlan& np = plans_[n];
@@ -921,8 +1046,8 @@ class Gen {
     const int NS = (int)np.sites.size();
     const int NR = (int)np.red_slots.size();
     o << "\nstruct P" << n << " { ";
-    if (np.staged) o << "alignas(64) unsigned char tm[128]; ";
-    o << "DkHdr h; " << (NR ? "DkPub pub; " : "") << "DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
+    if (np.staged && !np.sweep) o << "alignas(64) unsigned char tm[128]; ";
+    o << "DkHdr h; " << (NR ? "DkPub pub; " : "") << (np.sweep ? "DkUni u; " : "") << "DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_ << "_n" << n
       << "(const __grid_constant__ P" << n << " P) {\n";
@@ -941,6 +1066,10 @@ class Gen {
       for (int w : wslots) o << "  double w" << w << "_s = 0.0;\n";
       emit_scalar_seq(o, np, ne, /*apply_reduce=*/true, wslots);
       o << "}\n";
+      return;
+    }
+    if (np.sweep) {
+      nest_sweep(o, n, wslots);
       return;
     }
     if (np.staged) {
@@ -1485,12 +1614,14 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     memset(rd.data(), 0, sizeof(dk_view) * rd.size());
     for (int q = 0; q < NR; ++q) rd[q] = views[np.red_slots[q]];
     const size_t nsc = std::max(g.nscal, 1);
-    const size_t tmb = np.staged ? 128 : 0;  // CUtensorMap (64-byte aligned) leads a staged nest's params
-    size_t total = tmb + sizeof(DkHdr) + (NR ? sizeof(DkPub) : 0) + sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc;
-    if (np.staged) total = (total + 63) / 64 * 64;
+    const bool tma = np.staged && !np.sweep;
+    const size_t tmb = tma ? 128 : 0;  // CUtensorMap (64-byte aligned) leads a TMA-staged nest's params
+    size_t total = tmb + sizeof(DkHdr) + (NR ? sizeof(DkPub) : 0) + (np.sweep ? sizeof(DkUni) : 0) +
+                   sizeof(DkSite) * sites.size() + sizeof(dk_view) * rd.size() + 8 * nsc;
+    if (tma) total = (total + 63) / 64 * 64;
     blob.assign(total + 64, 0);
     char* p = blob.data();
-    if (np.staged) {
+    if (tma) {
       static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
       CUtensorMap tm;
       cuuint64_t gdim[2] = {(cuuint64_t)np.st_cols, (cuuint64_t)np.st_nrows};
@@ -1508,6 +1639,11 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     if (NR) {
       memcpy(p, &pb, sizeof pb);
       p += sizeof pb;
+    }
+    if (np.sweep) {
+      DkUni un = {np.st_base, np.st_rowstride, np.st_cols, np.st_nrows};
+      memcpy(p, &un, sizeof un);
+      p += sizeof un;
     }
     memcpy(p, sites.data(), sizeof(DkSite) * sites.size());
     p += sizeof(DkSite) * sites.size();
@@ -1540,7 +1676,14 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       tx = 32;
       ty = 1;
     }
-    if (np.staged) {
+    if (np.sweep) {
+      const int64_t ntask = ((((D[1] + 1) / 2) + 255) / 256) * ((D[0] + kSweepRows() - 1) / kSweepRows());
+      const int64_t cap = NR ? red_waves() * (int64_t)S.sm_count * m->occ[n] : 0x7fffffff;
+      gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntask, cap));
+      gy = 1;
+      tx = kTPB;
+      ty = 1;
+    } else if (np.staged) {
       const int64_t ntiles = ((D[0] + kTR - 1) / kTR) * ((D[1] + kTC - 1) / kTC);
       gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)S.sm_count * m->occ[n]));
       gy = 1;
