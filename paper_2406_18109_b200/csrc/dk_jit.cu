@@ -570,8 +570,9 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
     ks << "n" << n << ":r" << r << ":h" << np.shift << (np.oneshot ? "o" : "") << ":";
     // queue: stencil window 2.82 ms vs 3.20 ms with a cyclic tile walk (DK_K3_CYCLIC)
     np.st_queue = np.staged && getenv("DK_K3_CYCLIC") == nullptr;
+    const bool k3pref = getenv("DK_K3_NOPREF") == nullptr;
     if (np.sweep) np.st_queue = false;
-    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? "q" : "") << ";";
+    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? (k3pref ? "qp" : "q") : "") << ";";
     if (np.sweep) ks << "K3S:" << np.sw_np << "," << kSweepRows() << "," << kSweepAhead() << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
@@ -891,14 +892,25 @@ class Gen {
       // before its TMA (or a plain arrive once the queue is empty)
       o << "  __shared__ long long dk_tid[" << S << "];\n";
       o << "  unsigned int* const dk_q = (unsigned int*)P.h.red_ticket + 2;\n";
-      o << "  if (tid == 0)\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
+      // the ticket for the next refill is requested one iteration early
+      // (DK_K3_NOPREF=1 disables): its atomic round trip overlaps the current
+      // tile instead of holding every thread at the closing barrier.  Tickets
+      // grow per CTA, so the one left unused at exit is past the last tile.
+      const bool pref = getenv("DK_K3_NOPREF") == nullptr;
+      o << "  long long dk_pend = 0;\n";
+      o << "  if (tid == 0) {\n    for (int s = 0; s < " << S - 1 << "; ++s) {\n";
       o << "      const long long t = (long long)atomicAdd(dk_q, 1u); dk_tid[s] = t;\n";
       o << "      if (t < ntiles) " << tma("dk_smem(&dk_bar[s])", "dk_smem(&dk_tile[s][0][0])", "t")
         << " else dk_mbar_arrive(dk_smem(&dk_bar[s]));\n    }\n";
+      if (pref) o << "    dk_pend = (long long)atomicAdd(dk_q, 1u);\n";
+      o << "  }\n";
       o << "  for (int it = 0;; ++it) {\n";
       o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
       o << "    if (tid == 0) {\n      const int ns = (it + " << S - 1 << ") % " << S << ";\n";
-      o << "      const long long nxt = (long long)atomicAdd(dk_q, 1u); dk_tid[ns] = nxt;\n";
+      if (pref)
+        o << "      const long long nxt = dk_pend; dk_pend = (long long)atomicAdd(dk_q, 1u); dk_tid[ns] = nxt;\n";
+      else
+        o << "      const long long nxt = (long long)atomicAdd(dk_q, 1u); dk_tid[ns] = nxt;\n";
       o << "      dk_fence_proxy_async();\n";
       o << "      if (nxt < ntiles) " << tma("dk_smem(&dk_bar[ns])", "dk_smem(&dk_tile[ns][0][0])", "nxt")
         << " else dk_mbar_arrive(dk_smem(&dk_bar[ns]));\n    }\n";
