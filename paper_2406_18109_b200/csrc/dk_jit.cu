@@ -257,7 +257,8 @@ struct Site {
 // K3: aliased views of one store (the stencil's shifted interior views) are
 // staged tile by tile in shared memory by TMA and read from there; each
 // persistent CTA takes TR x TC output tiles from an atomic queue (in order
-// across the GPU) through an S-stage mbarrier ring.
+// across the GPU) through an S-stage mbarrier ring, refilled by a producer
+// warp (full/empty barriers) while 8 consumer warps compute.
 // output rows per tile (DK_K3_TR: 8, 12 or 16; thread t owns rows (t >> 6) + 4u)
 static int k_tr() {
   static int v = [] {
@@ -328,6 +329,7 @@ struct NestPlan {
   std::vector<int> red_slots;      // target slot per reduce statement (statement order)
   std::vector<char> red_is_array;  // per reduce statement
   int n_array_red = 0;
+  bool st_ws = false;  // K3 with a producer warp (full/empty mbarriers, no CTA barrier per tile)
   bool sweep = false;  // K3 as a register sweep (no TMA): see nest_sweep
   int sw_np = 1;       // union element pairs per row per thread
   int st_maxdr = 0;
@@ -571,8 +573,11 @@ static std::vector<NestPlan> plan_nests(const Prog& g, const dk_view* views, std
     // queue: stencil window 2.82 ms vs 3.20 ms with a cyclic tile walk (DK_K3_CYCLIC)
     np.st_queue = np.staged && getenv("DK_K3_CYCLIC") == nullptr;
     const bool k3pref = getenv("DK_K3_NOPREF") == nullptr;
+    // producer warp: stencil window 2.72 ms vs 2.85-2.88 ms with thread 0
+    // refilling between CTA barriers (same box; DK_K3_NOWS=1 restores that)
+    np.st_ws = np.st_queue && getenv("DK_K3_NOWS") == nullptr;
     if (np.sweep) np.st_queue = false;
-    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? (k3pref ? "qp" : "q") : "") << ";";
+    if (np.staged) ks << "K3:" << np.st_rows << "," << np.st_sh << "," << np.st_min_dc << (np.st_queue ? (k3pref ? "qp" : "q") : "") << (np.st_ws ? "w" : "") << ";";
     if (np.sweep) ks << "K3S:" << np.sw_np << "," << kSweepRows() << "," << kSweepAhead() << ";";
     for (const Site& s : np.sites) {
       if (s.staged) ks << "s" << s.dr << "," << s.dc;
@@ -851,10 +856,12 @@ class Gen {
     fail(DK_ERR_ARG, "bad expression");
   }
 
-  // K3: persistent CTAs walk kTR x kTC output tiles; thread 0 keeps the next
-  // tile's TMA load in flight (2 stages, one mbarrier each) while all 256
-  // threads compute the current one from shared memory.  Thread t owns the
-  // element pair (t & 63) of rows (t >> 6) and (t >> 6) + 4 of the tile.
+  // K3: persistent CTAs walk kTR x kTC output tiles through an S-stage ring.
+  // Default: a producer warp takes tickets from the queue and keeps S-1 TMA
+  // boxes in flight; 256 consumer threads compute from shared memory and
+  // release each stage per warp.  Without the producer warp (DK_K3_NOWS /
+  // DK_K3_CYCLIC) thread 0 refills between CTA barriers.  Consumer t owns the
+  // element pair (t & 63) of rows (t >> 6) + 4u of the tile.
   void nest_staged(std::ostringstream& o, int n, const std::vector<int>& wslots) const {
     const NestIR& ne = g_.nests[n];
     const NestPlan& np = plans_[n];
@@ -886,7 +893,29 @@ class Gen {
              " * " + std::to_string(kTR) + "), " + std::to_string(bytes) + "u);";
     };
     o << "  const int pr = tid & 63, rg = tid >> 6;\n";
-    if (np.st_queue) {
+    if (np.st_ws) {
+      // warp-specialised ring: warp 8 (one lane) takes tickets and issues the
+      // TMA refills as soon as the 8 consumer warps have released a stage
+      // (empty barrier, one arrive per warp); consumers only wait on the full
+      // barrier of their stage -- no CTA-wide barrier per tile
+      o << "  __shared__ __align__(8) unsigned long long dk_empty[" << S << "];\n";
+      o << "  __shared__ long long dk_tid[" << S << "];\n";
+      o << "  unsigned int* const dk_q = (unsigned int*)P.h.red_ticket + 2;\n";
+      o << "  if (tid == 0) {\n    for (int s = 0; s < " << S << "; ++s) dk_mbar_init(dk_smem(&dk_empty[s]), 8);\n";
+      o << "    dk_fence_mbar_init();\n  }\n  __syncthreads();\n";
+      o << "  if (tid >= " << kTPB << ") {\n    if (tid == " << kTPB << ") {\n";
+      o << "      long long pend = (long long)atomicAdd(dk_q, 1u);\n";
+      o << "      for (int it = 0;; ++it) {\n        const int s = it % " << S << ";\n";
+      o << "        if (it >= " << S << ") dk_mbar_wait(dk_smem(&dk_empty[s]), (uint32_t)(((it / " << S << ") - 1) & 1));\n";
+      o << "        const long long t = pend; dk_tid[s] = t;\n        dk_fence_proxy_async();\n";
+      o << "        if (t >= ntiles) { dk_mbar_arrive(dk_smem(&dk_bar[s])); break; }\n";
+      o << "        " << tma("dk_smem(&dk_bar[s])", "dk_smem(&dk_tile[s][0][0])", "t") << "\n";
+      o << "        pend = (long long)atomicAdd(dk_q, 1u);\n      }\n    }\n  } else\n";
+      o << "  for (int it = 0;; ++it) {\n";
+      o << "    const int stg = it % " << S << ";\n    const uint32_t ph = (uint32_t)((it / " << S << ") & 1);\n";
+      o << "    dk_mbar_wait(dk_smem(&dk_bar[stg]), ph);\n";
+      o << "    const int64_t tile = dk_tid[stg];\n    if (tile >= ntiles) break;\n";
+    } else if (np.st_queue) {
       // dynamic tile queue: tiles are handed out in order by an atomic ticket
       // (red_ticket[2]); the CTA's thread 0 publishes each stage's tile index
       // before its TMA (or a plain arrive once the queue is empty)
@@ -972,7 +1001,10 @@ class Gen {
       o << ");\n";
     }
     o << "      }\n    }\n";
-    o << "    __syncthreads();\n  }\n";
+    if (np.st_ws)
+      o << "    __syncwarp();\n    if ((tid & 31) == 0) dk_mbar_arrive(dk_smem(&dk_empty[stg]));\n  }\n";
+    else
+      o << "    __syncthreads();\n  }\n";
     if (np.st_queue) {
       // the last CTA out resets the queue for the next launch (stream order)
       o << "  if (tid == 0) {\n    __threadfence();\n    if (atomicAdd(dk_q + 1, 1u) == gridDim.x - 1) { dk_q[0] = 0u; dk_q[1] = 0u; }\n  }\n";
@@ -1061,7 +1093,7 @@ class Gen {
     if (np.staged && !np.sweep) o << "alignas(64) unsigned char tm[128]; ";
     o << "DkHdr h; " << (NR ? "DkPub pub; " : "") << (np.sweep ? "DkUni u; " : "") << "DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_ << "_n" << n
+    o << "extern \"C\" __global__ void __launch_bounds__(" << (np.st_ws ? kTPB + 32 : kTPB) << ", " << minb_ << ") " << name_ << "_n" << n
       << "(const __grid_constant__ P" << n << " P) {\n";
     // hoisted rank-0 operands
     for (int i = 0; i < NS; ++i)
@@ -1318,7 +1350,7 @@ class Gen {
     o << "  const int64_t G = (int64_t)gridDim.x * gridDim.y, blin = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;\n";
     o << "  double* red_part = (double*)P.h.red_part;\n";
     for (int a = 0; a < np.n_array_red; ++a)
-      o << "  { double v = dk_warp_sum(racc" << a << "); if (lane == 0) dk_sred[" << a << "][wid] = v; }\n";
+      o << "  { double v = dk_warp_sum(racc" << a << "); if (lane == 0 && wid < 8) dk_sred[" << a << "][wid] = v; }\n";
     o << "  __syncthreads();\n";
     o << "  if (lin == 0) {\n";
     for (int a = 0; a < np.n_array_red; ++a)
@@ -1331,11 +1363,11 @@ class Gen {
     o << "  double dk_tot[" << NA << "];\n";
     for (int a = 0; a < np.n_array_red; ++a) {
       // four independent accumulators keep four partial loads in flight per thread
-      o << "  { const double* rp = red_part + " << a << " * G; double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0; int64_t i = lin;\n"
+      o << "  { const double* rp = red_part + " << a << " * G; double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0; int64_t i = lin < 256 ? lin : G;\n"
         << "    #pragma unroll 1\n    for (; i + 768 < G; i += 1024) { s0 = dk_add(s0, dk_ldcg(rp + i)); s1 = dk_add(s1, dk_ldcg(rp + i + 256));"
         << " s2 = dk_add(s2, dk_ldcg(rp + i + 512)); s3 = dk_add(s3, dk_ldcg(rp + i + 768)); }\n"
         << "    #pragma unroll 1\n    for (; i < G; i += 256) s0 = dk_add(s0, dk_ldcg(rp + i));\n"
-        << "    double s = dk_add(dk_add(s0, s1), dk_add(s2, s3)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0) dk_sred[" << a << "][wid] = s; }\n";
+        << "    double s = dk_add(dk_add(s0, s1), dk_add(s2, s3)); s = dk_warp_sum(s); __syncthreads(); if (lane == 0 && wid < 8) dk_sred[" << a << "][wid] = s; }\n";
     }
     o << "  __syncthreads();\n";
     for (int a = 0; a < np.n_array_red; ++a)
@@ -1509,7 +1541,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
   for (size_t n = 0; n < k.prog.nests.size(); ++n) {
     CUfunction f = fns[n];
     int occ = 1;
-    DK_CU(cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kTPB, 0));
+    DK_CU(cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, plans[n].st_ws ? kTPB + 32 : kTPB, 0));
     occ = std::max(occ, 1);
     m->fn.push_back(f);
     m->occ.push_back(occ);
@@ -1699,7 +1731,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       const int64_t ntiles = ((D[0] + kTR - 1) / kTR) * ((D[1] + kTC - 1) / kTC);
       gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)S.sm_count * m->occ[n]));
       gy = 1;
-      tx = kTPB;
+      tx = np.st_ws ? kTPB + 32 : kTPB;
       ty = 1;
     }
     // one by-value struct parameter; the driver copies sizeof(P_n) bytes from the blob
