@@ -18,6 +18,7 @@ numpy executor on a bounded 1M-option sample).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -227,10 +228,15 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
     ex.sync()
     timed = seq[steady + warmup:]
     ev = []
+    # no cyclic-GC pauses inside the timed region (earlier workloads' traces
+    # leave millions of objects for a full collection to walk)
+    gc.collect()
+    gc.disable()
     n0 = ex.launch_count()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(ext_stream)
+    th0 = time.perf_counter()
     for i in timed:
         for k, e in its[i]:
             if k == "exec":
@@ -245,8 +251,11 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
             elif k == "free":
                 ex.free(e)
     end.record(ext_stream)
+    host_ms = (time.perf_counter() - th0) * 1e3  # host enqueue time of the K steps
     ex.sync()
+    gc.enable()
     ms = start.elapsed_time(end)
+    measure.host_ms = host_ms
     launches = ex.launch_count() - n0
     # dominant exec: largest summed device time
     per = {}
@@ -270,6 +279,17 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
             mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
             it_bytes += launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
     return ms, launches, dom, it_bytes
+
+
+def gather_all(torch, world, x):
+    if world == 1:
+        return [x]
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [round(float(o.item()), 4) for o in out]
 
 
 def reduce_max(torch, world, x):
@@ -354,8 +374,11 @@ def e2e_bs(ex, trace, steps, torch, ext_stream, world):
             replay(ex, step)
             ex.download_local(out, ho, rect)
     end.record(ext_stream)
+    host_ms = (time.perf_counter() - th0) * 1e3  # host enqueue time of the K steps
     ex.sync()
+    gc.enable()
     ms = start.elapsed_time(end)
+    measure.host_ms = host_ms
     # the chain's operator cycle is the identity: out == x + y exactly
     ok = bool(np.array_equal(ho[lo:hi], hx[lo:hi] + hy[lo:hi]))
     for p in ptrs:
@@ -459,8 +482,10 @@ def run_ours(args):
             ms, launches, dom, it_bytes = measure(ex, trace, steps or args.steps, args.warmup, torch, ext, rank)
             if sampler:
                 sampler.mark("t1")
+            per_rank = gather_all(torch, world, ms / (steps or args.steps))
+            host_rank = gather_all(torch, world, measure.host_ms / (steps or args.steps))
             ms = reduce_max(torch, world, ms)
-            res = {"ms": ms, "launches": launches, "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats),
+            res = {"ms": ms, "ranks_ms_per_step": per_rank, "host_ms_per_step": host_rank, "launches": launches, "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats),
                    "jit": ex.jit_stats()}
             if with_e2e:
                 e_ms, bi, bo, ok = e2e_bs(ex, trace, args.steps, torch, ext, world)
@@ -520,6 +545,8 @@ def run_ours(args):
         "hbm_gbs_step": round(main["it_bytes"] / (main["ms"] / K / 1e3) / 1e9, 1),
         "per_exec_ms": dom["per_exec_ms"] if dom else None,
         "gpu_launches": main["launches"],
+        "ranks_ms_per_step": main["ranks_ms_per_step"],
+        "host_enqueue_ms_per_step": main["host_ms_per_step"],
         "jit": main["jit"],
         "clocks": clocks,
     }
@@ -548,6 +575,8 @@ def run_ours(args):
                     "fused_iter_s": round(world * K / (f["ms"] / 1e3), 3),
                     "unfused_iter_s": round(world * K / (u["ms"] / 1e3), 3),
                     "fused_over_unfused": round(u["ms"] / f["ms"], 3),
+                    "fused_ranks_ms_per_step": f["ranks_ms_per_step"],
+                    "fused_host_enqueue_ms_per_step": f["host_ms_per_step"],
                     "fused_hbm_gbs_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9, 1),
                     "fused_hbm_frac_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9 / hbm_peak, 4),
                     "dominant": {"kind": d["kind"], "f": d["f"], "avg_ms": round(d["avg_ms"], 4),

@@ -182,8 +182,11 @@ void launch_builtin(const std::string& kind, const dk_view* v, int n, const int3
     // streaming nests, a grid covering the whole matrix keeps the HBM stream
     // tighter (0.862 vs 0.875 ms at 67M rows; DK_SPMV_PERSIST restores the
     // persistent grid).  Staging each CTA's nonzeros in shared memory first
-    // was measured slower (1.17 ms), and so was loading each row in predicated
-    // chunks of 8 (cols, vals, then the x gathers: 1.62 ms).
+    // was measured slower (1.17 ms), and so were loading each row in predicated
+    // chunks of 8 (cols, vals, then the x gathers: 1.62 ms) and a
+    // warp-cooperative layout (coalesced vals/cols over the warp's 32 rows,
+    // products staged in shared memory, per-row in-order sums: 1.46 ms).
+    // The per-row loop's strided loads are served from L1 (67 % hits).
     static const bool persist = getenv("DK_SPMV_PERSIST") != nullptr;
     const int blocks = (int)std::min<int64_t>((nrows + 255) / 256, persist ? (int64_t)sms * 8 : 0x7fffffff);
     if (rp.dtype == DK_I32)

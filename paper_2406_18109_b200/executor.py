@@ -80,6 +80,7 @@ class LaunchStats:
     transfers: int = 0
     inits: int = 0
     p2p_folds: int = 0  # reductions gathered through the peer-memory boards
+    mplan_hits: int = 0  # multi-GPU launches replayed from the plan cache
 
 
 class Executor:
@@ -115,6 +116,8 @@ class Executor:
         self._scal: dict[tuple, ctypes.Array] = {}
         self._acc: dict[int, tuple] = {}
         self._plans: dict[tuple, tuple] = {}  # launch-plan cache (one GPU)
+        self._mplans: dict[tuple, dict] = {}  # launch-plan cache (several GPUs), keyed on coherence state
+        self._rec: dict | None = None  # the multi-GPU plan being recorded by execute()
         self.stats = LaunchStats()
         self._comm = False
         self._p2p = False
@@ -174,6 +177,8 @@ class Executor:
     def _ensure(self, r: StoreRec, rect) -> None:
         if rg.empty(rect):
             return
+        if self._rec is not None:
+            self._rec["ensure"].append((r.sid, rect))
         self._device(r)
         lo, hi = rg.bbox_flat(r.shape, rect)
         check(self.lib.dk_store_ensure(r.sid, lo, hi))
@@ -346,6 +351,8 @@ class Executor:
                         if rest:
                             raise BackendError(f"coherence: store {sid} rect {rest[0]} valid nowhere")
                     r.valid[q] = rg.add(r.valid[q], want) if missing else r.valid[q]
+        if inits and self._rec is not None:
+            self._rec["inits"] = [(sid, list(rects)) for sid, rects in inits.items()]
         for sid, rects in inits.items():
             self._materialize_init(self.stores[sid], rects)
         mine = [t for t in transfers if self.rank in (t[2], t[3])]
@@ -371,6 +378,9 @@ class Executor:
                 self.stats.bytes_moved += rg.volume(rect) * r.esize
             self.stats.transfers += n
             check(self.lib.dk_comm_exchange(n, sids, peers, dirs, los, his))
+            if self._rec is not None:
+                nbytes = sum(rg.volume(t[1]) * self.stores[t[0]].esize for t in mine)
+                self._rec["xfer"] = (n, sids, peers, dirs, los, his, nbytes)
 
     def _wrote(self, sid: int, rect, q: int) -> None:
         r = self.stores[sid]
@@ -435,7 +445,8 @@ class Executor:
         if kp is None and task.kind not in BUILTIN_KINDS:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
-        if kp is not None and self.world == 1:
+        use_mplan = os.environ.get("DK_MPLAN", "1") != "0"
+        if kp is not None and self.world == 1 and not use_mplan:
             # key on the non-temporary arguments: each memo replay of a window names fresh
             # temporaries, which never reach the device
             pkey = (id(kp), task.launch, temp_positions, task.scalars,
@@ -451,6 +462,161 @@ class Executor:
                 self.stats.launches += 1
                 self.stats.points += len(hit[2])
                 return
+        if use_mplan:
+            key, sids = self._mplan_key(task, kp, temp_positions)
+            hit = self._mplans.get(key) if key is not None else None
+            if hit is not None and hit["kp"] is kp:
+                self._mplan_replay(hit, task, kp, sids)
+                return
+            self._rec = {"ok": key is not None, "xfer": None, "views": [], "fold": [], "pub": False,
+                         "ensure": [], "inits": []}
+            try:
+                self._execute_planned(task, kp, temp_positions, None)
+                if self._rec["ok"]:
+                    self._mplan_store(key, sids, kp)
+            finally:
+                self._rec = None
+            return
+        self._execute_planned(task, kp, temp_positions, pkey if kp is not None and self.world == 1 else None)
+        # (DK_MPLAN=0: the round-1 plan cache -- one GPU, exact arguments only)
+
+    # ------------------------------------------------ multi-GPU plan cache
+    # A memo-replayed window repeats with the same launch, the same coherence
+    # state of its stores (valid / written rects per rank) and -- for the
+    # per-iteration scalars of CG -- fresh rank-0 stores in the same roles.
+    # Stores are therefore keyed by their first-appearance index in the task's
+    # arguments; the recorded transfers, initialisations, bindings (pointer =
+    # store base + offset), fold and post-launch coherence state are replayed
+    # onto the actual stores.  Every rank holds the same replicated state, so
+    # every rank hits or misses together.
+    def _mplan_key(self, task, kp, temp_positions):
+        sids = []
+        for j, a in enumerate(task.args):
+            if j not in temp_positions and a.store not in sids:
+                sids.append(a.store)
+        sig = []
+        for sid in sids:
+            r = self.rec(sid)
+            sig.append((r.shape, r.dtype, tuple(tuple(v) for v in r.valid), tuple(r.written),
+                        sid if r.shape else None))  # large stores by identity, rank-0 ones by role
+        cidx = {sid: c for c, sid in enumerate(sids)}
+        args = tuple((cidx[a.store], a.part, a.priv) if j not in temp_positions else None
+                     for j, a in enumerate(task.args))
+        kid = id(kp) if kp is not None else task.kind
+        return (kid, task.launch, temp_positions, task.scalars, args, tuple(sig)), sids
+
+    def _mplan_store(self, key, sids, kp) -> None:
+        rec = self._rec
+        cidx = {sid: c for c, sid in enumerate(sids)}
+        base = {sid: self.stores[sid].base for sid in sids if sid in self.stores}
+
+        def canon_views(views, slots):
+            out = []
+            for idx, sid in slots:
+                if sid not in cidx or sid not in base:
+                    return None
+                v = views if idx is None else views[idx]
+                out.append((idx, cidx[sid], v.ptr - base[sid]))
+            return (views, out)
+
+        plan = {"kp": kp, "pub": rec["pub"], "counts": rec.get("counts")}
+        vs = []
+        for item in rec["views"]:
+            if kp is None:
+                (views, slots), n, wflags = item
+                cv = canon_views(views, slots)
+                vs.append(None if cv is None else (cv, n, wflags))
+            else:
+                vs.append(canon_views(*item))
+        fold = []
+        for (tv, slots), first, stride, n in rec["fold"]:
+            cv = canon_views(tv, slots)
+            fold.append(None if cv is None else (cv, first, stride, n))
+        if any(v is None for v in vs) or any(f is None for f in fold):
+            return
+        if any(sid not in cidx for sid, _ in rec["ensure"]) or any(sid not in cidx for sid, _ in rec["inits"]):
+            return
+        plan["views"], plan["fold"] = vs, fold
+        dev = set()
+        for item in vs:
+            cv = item[0] if kp is None else item
+            dev.update(c for _, c, _ in cv[1])
+        for cv, *_ in fold:
+            dev.update(c for _, c, _ in cv[1])
+        plan["dev"] = sorted(dev)
+        plan["ensure"] = sorted({(cidx[sid], rect) for sid, rect in rec["ensure"]})
+        plan["inits"] = [(cidx[sid], rects) for sid, rects in rec["inits"]]
+        x = rec["xfer"]
+        if x is not None:
+            n, xs, peers, dirs, los, his, nbytes = x
+            if any(xs[i] not in cidx for i in range(n)):
+                return
+            x = (n, [cidx[xs[i]] for i in range(n)], peers, dirs, los, his, nbytes)
+        plan["xfer"] = x
+        plan["post"] = tuple((c, tuple(tuple(v) for v in self.stores[sid].valid), tuple(self.stores[sid].written))
+                             for c, sid in enumerate(sids))
+        if len(self._mplans) > 4096:
+            self._mplans.clear()
+        self._mplans[key] = plan
+
+    @staticmethod
+    def _rebind(cv, bases):
+        views, patches = cv
+        if patches and patches[0][0] is None:  # a single view
+            nv = dk_view()
+            ctypes.pointer(nv)[0] = views
+            nv.ptr = bases[patches[0][1]] + patches[0][2]
+            return nv
+        nv = (dk_view * len(views))()
+        ctypes.memmove(nv, views, ctypes.sizeof(views))
+        for idx, c, off in patches:
+            nv[idx].ptr = bases[c] + off
+        return nv
+
+    def _mplan_replay(self, hit, task, kp, sids) -> None:
+        recs = [self.rec(sid) for sid in sids]
+        for c, rects in hit["inits"]:
+            self._materialize_init(recs[c], rects)
+        for c, rect in hit["ensure"]:
+            self._ensure(recs[c], rect)
+        for c in hit["dev"]:
+            self._device(recs[c])
+        bases = [r.base for r in recs]
+        x = hit["xfer"]
+        if x is not None:
+            n, cs, peers, dirs, los, his, nbytes = x
+            check(self.lib.dk_comm_exchange(n, (c_int64 * n)(*[sids[c] for c in cs]), peers, dirs, los, his))
+            self.stats.transfers += n
+            self.stats.bytes_moved += nbytes
+        if kp is None:
+            kind = task.kind.encode()
+            for cv, n, wflags in hit["views"]:
+                check(self.lib.dk_builtin(kind, self._rebind(cv, bases), n, wflags))
+        else:
+            h, _ = self.kernel_handle(kp)
+            scal = self._scalars(task.scalars)
+            ns, nsl = len(task.scalars), len(kp.slots)
+            if hit["pub"]:
+                slot = self._p2p_epoch % runtime.P2P_SLOTS
+                self._p2p_epoch += 1
+                for sir, cv in enumerate(hit["views"]):
+                    check(self.lib.dk_launch_pub(h, self._rebind(cv, bases), nsl, scal, ns, slot, sir))
+                g = c_uint64()
+                check(self.lib.dk_p2p_wait(slot, hit["counts"], byref(g)))
+                for cv, first, stride, nv in hit["fold"]:
+                    check(self.lib.dk_accum(byref(self._rebind(cv, bases)), g.value, first, stride, nv))
+                self.stats.p2p_folds += 1
+            else:
+                for cv in hit["views"]:
+                    check(self.lib.dk_launch(h, self._rebind(cv, bases), nsl, scal, ns, 0))
+        for c, valid, written in hit["post"]:
+            recs[c].valid = [list(v) for v in valid]
+            recs[c].written = list(written)
+        self.stats.launches += 1
+        self.stats.points += len(hit["views"])
+        self.stats.mplan_hits += 1
+
+    def _execute_planned(self, task: TaskDesc, kp: KProg | None, temp_positions, pkey) -> None:
         pts = list(task.points())
         V = len(pts)
         prank = [self.point_rank(i, V) for i in range(V)]
@@ -511,7 +677,7 @@ class Executor:
             self._run_builtin(task, pts, mine, rects, prank)
         else:
             recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
-            if recorded is not None and self.world == 1:
+            if recorded is not None and self.world == 1 and pkey is not None:
                 # launch-plan cache: a memo-replayed window over the same
                 # stores re-launches with the bound views as they are
                 if len(self._plans) > 4096:
@@ -640,6 +806,12 @@ class Executor:
             check(self.lib.dk_memset_zero(totals, nbytes * (self.world + 1)))
         has_local = any(s.local for s in kp.slots)
         recorded = [] if not (use_totals or has_local or pub_slot >= 0) else None
+        if self._rec is not None:
+            if use_totals or has_local:
+                self._rec["ok"] = False
+            elif pub_slot >= 0:
+                self._rec["pub"] = True
+                self._rec["counts"] = (c_int32 * self.world)(*counts)
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * nslots)()
             rp = rects[i]
@@ -678,6 +850,9 @@ class Executor:
                 check(self.lib.dk_scratch_free(p))
             if recorded is not None:
                 recorded.append(views)
+            if self._rec is not None:
+                self._rec["views"].append((views, [
+                    (si, task.args[s.arg].store) for si, s in enumerate(kp.slots) if not s.local]))
         if use_totals:
             block = maxp * nred
             gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
@@ -690,6 +865,11 @@ class Executor:
             self._fold(task, kp, prank, rects, red_targets, g.value, runtime.P2P_POINTS, nred)
             self.stats.p2p_folds += 1
         return recorded
+
+    def _accum(self, sid, tv, gathered, first, stride, n) -> None:
+        check(self.lib.dk_accum(byref(tv), gathered, first, stride, n))
+        if self._rec is not None:
+            self._rec["fold"].append(((tv, [(None, sid)]), first, stride, n))
 
     def _fold(self, task, kp, prank, rects, red_targets, gathered, maxp, nred) -> None:
         """Fold gathered per-point totals ([world][maxp][nred]) in lexicographic point order."""
@@ -712,17 +892,17 @@ class Executor:
                     ks = [idx[i][k] for i in range(V)]
                     stride = ks[1] - ks[0] if V > 1 else 1
                     if all(ks[t] == ks[0] + t * stride for t in range(V)):
-                        check(self.lib.dk_accum(byref(tv), gathered, ks[0], stride, V))
+                        self._accum(a.store, tv, gathered, ks[0], stride, V)
                     else:
                         for kk in ks:
-                            check(self.lib.dk_accum(byref(tv), gathered, kk, 1, 1))
+                            self._accum(a.store, tv, gathered, kk, 1, 1)
                 else:
                     for i in range(V):
                         if prank[i] != self.rank:
                             continue
                         r = self.stores[a.store]
                         tv = self.view(r, rects[i][s.arg])
-                        check(self.lib.dk_accum(byref(tv), gathered, idx[i][k], 1, 1))
+                        self._accum(a.store, tv, gathered, idx[i][k], 1, 1)
             return
         for i in range(V):
             for k, (sl, s) in enumerate(red_targets):
@@ -733,7 +913,7 @@ class Executor:
                 rect = r.full if a.part.is_none else rects[i][s.arg]
                 self._ensure(r, rect)
                 tv = self.view(r, rect)
-                check(self.lib.dk_accum(byref(tv), gathered, idx[i][k], 1, 1))
+                self._accum(a.store, tv, gathered, idx[i][k], 1, 1)
 
     def _run_builtin(self, task, pts, mine, rects, prank) -> None:
         n = len(task.args)
@@ -741,6 +921,8 @@ class Executor:
         kind = task.kind.encode()
         red = [j for j, a in enumerate(task.args) if a.reduces]
         arenas = self.world > 1 and bool(red)
+        if arenas and self._rec is not None:
+            self._rec["ok"] = False
         if arenas:
             # per-point zero arenas for the Rd args (executor.py:280-281), then the
             # same allgather + point-order fold as kernel reductions
@@ -769,6 +951,8 @@ class Executor:
                 self._ensure(r, rects[i][j])
                 views[j] = self.view(r, rects[i][j])
             check(self.lib.dk_builtin(kind, views, n, wflags))
+            if self._rec is not None:
+                self._rec["views"].append(((views, [(j, a.store) for j, a in enumerate(task.args)]), n, wflags))
         if arenas:
             gathered = tb.value + 8 * block
             check(self.lib.dk_comm_allgather_f64(tb.value + 8 * block * self.rank, gathered, block))

@@ -107,7 +107,7 @@ with gzip.open(os.path.join(T.GOLDEN, "plans_medium.json.gz"), "rt") as f:
 n = 0
 for tr in traces:
     name = tr.meta["name"]
-    if not name.startswith("stencil"):
+    if not name.startswith(tuple(os.environ.get("DK_VARIANT_PLANS", "stencil").split(","))):
         continue
     got, _ = T._run(Executor, tr)
     ref = oracle_replay(tr)
@@ -135,6 +135,21 @@ def test_stencil_codegen_variants_match_oracle(variant, tmp_path):
                          timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "checked 12" in out.stdout
+
+
+@pytest.mark.parametrize("variant", ["DK_SPMV_PERSIST"])
+def test_spmv_variants_match_oracle(variant, tmp_path):
+    """CG / PCG plans with the persistent-grid SPMV_CSR kernel."""
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DK_REPO=repo, DK_JIT_CACHE=str(tmp_path), DK_VARIANT_PLANS="cg,pcg")
+    env[variant] = "1"
+    out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "checked 0" not in out.stdout
 
 
 def test_cg_residual_history(Executor):
