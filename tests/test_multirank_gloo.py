@@ -41,6 +41,7 @@ def _worker(rank, world, port, names, q, p2p=False):
     cases = {c["name"]: c for c in load_golden("bench_small.json.gz") + load_golden("fuzz250.json.gz")}
     bad = []
     moved = 0
+    hits = 0
     for name in names:
         if isinstance(name, dict):  # synthetic trace: compare with the oracle instead of a golden heap
             from oracle.interp import replay as oreplay
@@ -65,6 +66,7 @@ def _worker(rank, world, port, names, q, p2p=False):
             replay(ex, trace.events)
             got = {s: ex.get(s) for s in trace.live}
             moved += ex.stats.p2p_folds if p2p else ex.stats.transfers
+            hits += ex.stats.mplan_hits
             if rank == 0:
                 want = want_arrays if want_arrays is not None else golden_arrays(case)
                 for s, w in want.items():
@@ -73,7 +75,7 @@ def _worker(rank, world, port, names, q, p2p=False):
         except Exception as e:  # noqa: BLE001
             bad.append((name, f"{type(e).__name__}: {e}"))
             break  # the peer may be blocked in a collective: stop instead of desynchronising
-    q.put((rank, bad, moved))
+    q.put((rank, bad, moved, hits))
     dist.destroy_process_group()
 
 
@@ -107,10 +109,12 @@ MULTI_POINT = [
 
 def test_benchmarks_two_ranks_match_reference():
     res = _run(MULTI_POINT)
-    bad = [b for _, bs, _ in res for b in bs]
+    bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
     # the multi-point stencils and the CSR CG need halos / replicated reads
     assert res[0][2] > 0 and res[1][2] > 0
+    # steady iterations replay through the coherence-keyed launch-plan cache
+    assert res[0][3] > 0 and res[1][3] > 0
 
 
 def test_peer_board_reductions_match_reference():
@@ -121,9 +125,9 @@ def test_peer_board_reductions_match_reference():
              "cg_like/fused", "stencil/fused", "edge_empty_tiles/fused", "edge_rank0/fused", "edge_ragged_2d/fused"]
     for world in (2, 3):
         res = _run(names, world=world, p2p=True)
-        bad = [b for _, bs, _ in res for b in bs]
+        bad = [b for _, bs, *_ in res for b in bs]
         assert not bad, bad[:10]
-        assert all(folds > 0 for _, _, folds in res), res
+        assert all(r[2] > 0 for r in res), res
 
 
 def test_uneven_point_mapping_three_ranks():
@@ -131,7 +135,7 @@ def test_uneven_point_mapping_three_ranks():
     names = ["stencil_bands_n6_k4/fused", "cg_csr_6x12_k4/fused", "cg_csr_6x12_k4/unfused",
              "blackscholes_chain/fused", "stencil/fused", "cg_like/fused"]
     res = _run(names, world=3)
-    bad = [b for _, bs, _ in res for b in bs]
+    bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
 
 
@@ -151,7 +155,7 @@ def _norm_trace():
 
 def test_builtin_reductions_two_ranks():
     res = _run([_norm_trace()])
-    bad = [b for _, bs, _ in res for b in bs]
+    bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad
 
 
@@ -159,5 +163,5 @@ def test_builtin_reductions_two_ranks():
 def test_fuzz_corpus_two_ranks_match_reference():
     names = [f"fuzz{s}/{c}" for s in range(0, 250, 2) for c in ("fused", "unfused")]
     res = _run(names)
-    bad = [b for _, bs, _ in res for b in bs]
+    bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
