@@ -22,11 +22,34 @@ def _codes(co):
             yield from _codes(c)
 
 
-def test_bench_globals_resolve():
-    path = os.path.join(REPO, "bench.py")
-    spec = importlib.util.spec_from_file_location("bench_static", path)
+import importlib
+
+import pytest
+
+
+def _load(rel):
+    path = os.path.join(REPO, rel)
+    if rel.endswith("session.py"):
+        ref = os.path.join(REPO, "baseline", "_ref")
+        if not os.path.isdir(os.path.join(ref, "diffusekit")):
+            pytest.skip("reference not installed (baseline/_ref)")
+        import sys
+
+        if ref not in sys.path:
+            sys.path.append(ref)
+    if rel.startswith("paper_2406_18109_b200/"):
+        return path, importlib.import_module(rel[:-3].replace("/", "."))
+    spec = importlib.util.spec_from_file_location(rel.replace("/", "_")[:-3] + "_static", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
+    return path, mod
+
+
+@pytest.mark.parametrize("rel", ["bench.py", "__graft_entry__.py", "paper_2406_18109_b200/executor.py",
+                                 "paper_2406_18109_b200/streaming.py", "paper_2406_18109_b200/session.py",
+                                 "paper_2406_18109_b200/runtime.py", "tools/host_overhead.py"])
+def test_globals_resolve(rel):
+    path, mod = _load(rel)
     src = open(path).read()
     top = compile(src, path, "exec")
     missing = set()
