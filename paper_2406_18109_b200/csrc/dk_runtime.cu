@@ -265,7 +265,10 @@ int dk_store_free(int64_t sid) {
     // order makes the reuse safe); bound the pool so it cannot hoard HBM
     size_t mapped = 0;
     for (auto& m : s.maps) mapped += m.size;
-    const size_t kPoolCap = (size_t)64 << 30;
+    static const size_t kPoolCap = [] {
+      const char* e = getenv("DK_VA_POOL_GB");  // 0 disables the pool
+      return (size_t)(e ? atoll(e) : 64) << 30;
+    }();
     if (S.pool_bytes + mapped > kPoolCap) {
       DK_CUDA(cudaStreamSynchronize(S.stream));
       release_large(s);

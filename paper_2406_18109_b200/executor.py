@@ -446,7 +446,8 @@ class Executor:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
         use_mplan = os.environ.get("DK_MPLAN", "1") != "0"
-        if kp is not None and self.world == 1 and not use_mplan:
+        pkey = None
+        if kp is not None and self.world == 1:
             # key on the non-temporary arguments: each memo replay of a window names fresh
             # temporaries, which never reach the device
             pkey = (id(kp), task.launch, temp_positions, task.scalars,
@@ -471,14 +472,13 @@ class Executor:
             self._rec = {"ok": key is not None, "xfer": None, "views": [], "fold": [], "pub": False,
                          "ensure": [], "inits": []}
             try:
-                self._execute_planned(task, kp, temp_positions, None)
+                self._execute_planned(task, kp, temp_positions, pkey)
                 if self._rec["ok"]:
                     self._mplan_store(key, sids, kp)
             finally:
                 self._rec = None
             return
-        self._execute_planned(task, kp, temp_positions, pkey if kp is not None and self.world == 1 else None)
-        # (DK_MPLAN=0: the round-1 plan cache -- one GPU, exact arguments only)
+        self._execute_planned(task, kp, temp_positions, pkey)
 
     # ------------------------------------------------ multi-GPU plan cache
     # A memo-replayed window repeats with the same launch, the same coherence
