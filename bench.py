@@ -216,8 +216,9 @@ def reference_session_rate(size, budget_s=None, warmup=3, steps=None):
     return n / dt, n, dt
 
 
-def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True):
-    """Warm-up W iterations past the ramp, then time exactly K iterations on the executor's stream."""
+def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True, sync_ranks=None):
+    """Warm-up W iterations past the ramp, then time exactly K iterations on the executor's stream,
+    bracketed by ``sync_ranks`` (barrier + device synchronize on every rank) on both sides."""
     from paper_2406_18109_b200.executor import replay
     from paper_2406_18109_b200.traffic import launch_bytes
 
@@ -226,6 +227,8 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
     for i in seq[: steady + warmup]:
         replay(ex, its[i])
     ex.sync()
+    if sync_ranks is not None:
+        sync_ranks()  # every rank starts its timed region together (warm-up lengths differ)
     timed = seq[steady + warmup:]
     ev = []
     # no cyclic-GC pauses inside the timed region (earlier workloads' traces
@@ -253,6 +256,8 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True)
     end.record(ext_stream)
     host_ms = (time.perf_counter() - th0) * 1e3  # host enqueue time of the K steps
     ex.sync()
+    if sync_ranks is not None:
+        sync_ranks()
     gc.enable()
     ms = start.elapsed_time(end)
     measure.host_ms = host_ms
@@ -476,7 +481,12 @@ def run_ours(args):
             barrier(torch, world)
             if sampler:
                 sampler.mark("t0")
-            ms, launches, dom, it_bytes = measure(ex, trace, steps or args.steps, args.warmup, torch, ext, rank)
+            def sync_ranks():
+                barrier(torch, world)
+                torch.cuda.synchronize()
+
+            ms, launches, dom, it_bytes = measure(ex, trace, steps or args.steps, args.warmup, torch, ext, rank,
+                                                  sync_ranks=sync_ranks)
             if sampler:
                 sampler.mark("t1")
             per_rank = gather_all(torch, world, ms / (steps or args.steps))
