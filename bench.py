@@ -511,6 +511,10 @@ def run_ours(args):
     wl = args.workload
     if args.quick:
         args.no_extra = True
+    for spec in filter(None, (args.pre or "").split(",")):
+        # diagnostics: run other workloads in this process first ("stencil" or "stencil:unfused")
+        w2, _, mode2 = spec.partition(":")
+        one(w2, mode2 or "fused")
     main = one(wl, "fused", with_clock=True, with_e2e=(wl == "bs" and not args.quick))
     clocks = one.clock
     K = args.steps
@@ -678,6 +682,7 @@ def main():
     ap.add_argument("--workload", default="bs", choices=list(WORKLOADS))
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--quick", action="store_true", help="headline device timing only (no e2e, extras, CPU baseline)")
+    ap.add_argument("--pre", default="", help="diagnostics: workloads to run in this process before the timed one")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
