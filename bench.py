@@ -328,6 +328,50 @@ def make_executor(trace, rank, world, local, torch):
     return ex
 
 
+def measure_graph(ex, trace, steps, warmup, torch, ext_stream):
+    """configs[0] through a CUDA graph: warm up past the ramp, capture ONE
+    memo-replayed steady iteration from the library stream, then time ``steps`` launches of
+    that graph with CUDA events.  The device work per step is the iteration's own kernels
+    (same bindings); only the per-window host dispatch is gone.  Checks out == x + y after."""
+    import numpy as np
+
+    from paper_2406_18109_b200.executor import replay
+
+    its, steady = iteration_split(trace)
+    seq = list(range(steady)) + [steady + (i % (len(its) - steady)) for i in range(warmup + 1)]
+    for i in seq[:-1]:
+        replay(ex, its[i])
+    ex.sync()
+    step = its[seq[-1]]
+    execs = [e for k, e in step if k == "exec"]
+    t = execs[0].task
+    xs, ys = t.args[0].store, t.args[1].store
+    out = [a.store for e in execs for a in e.task.args if a.priv == "W" and a.store in trace.live][-1]
+    g = ex.capture(lambda: replay(ex, step))
+    try:
+        check_fill = ex.lib.dk_store_fill(out, 0, int(np.prod(trace.shapes[out])), float("nan"))
+        if check_fill != 0:
+            raise RuntimeError("dk_store_fill failed")
+        for _ in range(warmup):
+            ex.graph_launch(g)
+        ex.sync()
+        n0 = ex.launch_count()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(ext_stream)
+        for _ in range(steps):
+            ex.graph_launch(g)
+        end.record(ext_stream)
+        ex.sync()
+        ms = start.elapsed_time(end)
+        launches = ex.launch_count() - n0
+        x, y, o = ex.download(xs), ex.download(ys), ex.download(out)
+        ok = bool(np.array_equal(o, x + y))
+    finally:
+        ex.graph_destroy(g)
+    return ms, launches, ok
+
+
 def e2e_bs(ex, trace, steps, torch, ext_stream, world):
     """Same iteration through the executor with host buffers: H2D(x, y) + fused step + D2H(out)."""
     import ctypes
@@ -606,6 +650,19 @@ def run_ours(args):
                                         "note": "device-timed 200 replayed iterations; host enqueue bound at this size"}
             except Exception as exc:  # noqa: BLE001
                 out["c1_1M_options"] = {"error": f"{type(exc).__name__}: {exc}"}
+            try:
+                ex1 = make_executor(load_trace("bs_fused_c1"), rank, world, local, torch)
+                try:
+                    g_ms, g_l, g_ok = measure_graph(ex1, load_trace("bs_fused_c1"), 200, args.warmup, torch,
+                                                    torch.cuda.ExternalStream(ex1.stream()))
+                finally:
+                    ex1.close()
+                out["c1_1M_options"]["graph"] = {
+                    "fused_iter_s": round(200 / (g_ms / 1e3), 1), "ms_per_step": round(g_ms / 200, 4),
+                    "gpu_launches": g_l, "result_check": "out == x + y" if g_ok else "FAILED",
+                    "note": "one captured steady iteration relaunched as a CUDA graph 200 times (dk_graph_*)"}
+            except Exception as exc:  # noqa: BLE001
+                out["c1_1M_options"]["graph"] = {"error": f"{type(exc).__name__}: {exc}"}
     if wl == "bs" and not args.no_extra:
         try:
             out["gpusession"] = run_gpusession(args.steps, rank, world, local)

@@ -109,6 +109,15 @@ int dk_stream_wait_event(uint64_t event);  /* current stream waits */
 int dk_event_sync(uint64_t event);
 int dk_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 
+/* CUDA graphs (no reference counterpart — the reference re-runs
+ * Session._replay, pipeline.py:278-286, per memo hit): capture the library
+ * stream's work between begin/end (e.g. one memo-replayed iteration whose
+ * launches are prepared) and relaunch it as one graph on the current stream. */
+int dk_graph_begin(void);
+int dk_graph_end(uint64_t* graph);
+int dk_graph_launch(uint64_t graph);
+int dk_graph_destroy(uint64_t graph);
+
 /* JIT: program text (paper_2406_18109_b200.ir.KProg.wire) -> handle.
  * Compilation to sm_100a happens at first launch per binding class. */
 int dk_kernel_compile(const char* program, int64_t len, int64_t* handle);

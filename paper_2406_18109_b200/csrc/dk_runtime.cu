@@ -517,3 +517,70 @@ int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t
 }
 
 }  // extern "C"
+
+// ---- CUDA graphs of memo-hit windows --------------------------
+// A replayed iteration whose launches are already in the prepared-launch cache
+// is captured once from the library stream and relaunched as one graph: the
+// device work is identical (same kernels, bindings and transfers), the host
+// pays one cudaGraphLaunch instead of the front end's per-window dispatch.
+
+namespace {
+struct GraphRec {
+  cudaGraphExec_t exec;
+  int64_t kernels;
+};
+std::unordered_map<uint64_t, GraphRec> g_graphs;
+uint64_t g_next_graph = 1;
+int64_t g_capture_launch0 = -1;
+}  // namespace
+
+extern "C" {
+
+int dk_graph_begin(void) {
+  return guard([&] {
+    require_init();
+    if (g_capture_launch0 >= 0) fail(DK_ERR_ARG, "a graph capture is already open");
+    DK_CUDA(cudaStreamBeginCapture(st().stream, cudaStreamCaptureModeRelaxed));
+    g_capture_launch0 = st().launches;
+  });
+}
+
+int dk_graph_end(uint64_t* graph) {
+  return guard([&] {
+    require_init();
+    if (g_capture_launch0 < 0) fail(DK_ERR_ARG, "no graph capture is open");
+    const int64_t k = st().launches - g_capture_launch0;
+    g_capture_launch0 = -1;
+    st().launches -= k;  // captured, not launched
+    cudaGraph_t g = nullptr;
+    DK_CUDA(cudaStreamEndCapture(st().stream, &g));
+    cudaGraphExec_t e = nullptr;
+    cudaError_t r = cudaGraphInstantiate(&e, g, 0);
+    cudaGraphDestroy(g);
+    DK_CUDA(r);
+    const uint64_t id = g_next_graph++;
+    g_graphs[id] = GraphRec{e, k};
+    *graph = id;
+  });
+}
+
+int dk_graph_launch(uint64_t graph) {
+  return guard([&] {
+    require_init();
+    auto it = g_graphs.find(graph);
+    if (it == g_graphs.end()) fail(DK_ERR_ARG, "unknown graph %llu", (unsigned long long)graph);
+    DK_CUDA(cudaGraphLaunch(it->second.exec, st().stream));
+    st().launches += it->second.kernels;
+  });
+}
+
+int dk_graph_destroy(uint64_t graph) {
+  return guard([&] {
+    auto it = g_graphs.find(graph);
+    if (it == g_graphs.end()) fail(DK_ERR_ARG, "unknown graph %llu", (unsigned long long)graph);
+    DK_CUDA(cudaGraphExecDestroy(it->second.exec));
+    g_graphs.erase(it);
+  });
+}
+
+}  // extern "C"

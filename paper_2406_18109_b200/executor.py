@@ -1037,6 +1037,25 @@ class Executor:
         check(self.lib.dk_launch_count(byref(n)))
         return n.value
 
+    def capture(self, fn) -> int:
+        """Run ``fn()`` (enqueue-only executor calls, e.g. one memo-replayed iteration whose
+        launches are already planned) under stream capture; returns a graph handle for
+        :meth:`graph_launch`.  Any synchronising call inside ``fn`` fails the capture."""
+        check(self.lib.dk_graph_begin())
+        g = c_uint64()
+        try:
+            fn()
+        finally:
+            rc = self.lib.dk_graph_end(byref(g))
+        check(rc)
+        return g.value
+
+    def graph_launch(self, graph: int) -> None:
+        check(self.lib.dk_graph_launch(c_uint64(graph)))
+
+    def graph_destroy(self, graph: int) -> None:
+        check(self.lib.dk_graph_destroy(c_uint64(graph)))
+
     def stream(self) -> int:
         s = c_uint64()
         check(self.lib.dk_get_stream(byref(s)))

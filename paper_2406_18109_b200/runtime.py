@@ -48,6 +48,10 @@ _SIGS = {
     "dk_sync": (c_int, []),
     "dk_device_info": (c_int, [POINTER(c_int), POINTER(c_int64), POINTER(c_int64)]),
     "dk_launch_count": (c_int, [POINTER(c_int64)]),
+    "dk_graph_begin": (c_int, []),
+    "dk_graph_end": (c_int, [POINTER(c_uint64)]),
+    "dk_graph_launch": (c_int, [c_uint64]),
+    "dk_graph_destroy": (c_int, [c_uint64]),
     "dk_store_create": (c_int, [c_int64, c_int, POINTER(c_int64), c_int]),
     "dk_store_ensure": (c_int, [c_int64, c_int64, c_int64]),
     "dk_store_free": (c_int, [c_int64]),
