@@ -211,7 +211,7 @@ int dk_p2p_init(int* enabled) {
     cudaIpcMemHandle_t mine;
     memset(&mine, 0, sizeof mine);
     if (ok) ok = cudaMalloc(&S.board, kP2PBoardBytes) == cudaSuccess;
-    if (ok) ok = cudaMemset(S.board, 0, kP2PBoardBytes) == cudaSuccess;
+    if (ok) ok = cudaMemsetAsync(S.board, 0, kP2PBoardBytes, s) == cudaSuccess;
     if (ok) ok = cudaIpcGetMemHandle(&mine, S.board) == cudaSuccess;
     cudaGetLastError();
     // all-gather the IPC handles (and the success bits) over NCCL
@@ -263,6 +263,7 @@ int dk_p2p_init(int* enabled) {
 int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered) {
   return guard([&] {
     require_init();
+    require_not_capturing("dk_p2p_wait");
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
     if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);

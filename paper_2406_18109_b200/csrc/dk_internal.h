@@ -91,6 +91,8 @@ struct State {
   std::multimap<size_t, Store> va_pool;  // freed large stores kept mapped, by va_size
   size_t pool_bytes = 0;
   int64_t launches = 0;
+  // >= 0 while a CUDA-graph capture is open on `stream` (launch count at dk_graph_begin)
+  int64_t capture_launch0 = -1;
   // collectives
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -111,6 +113,10 @@ constexpr size_t kP2PBoardBytes = DK_P2P_SLOTS * (kP2PSlotBytes + kP2PFlagBytes)
 
 State& st();
 void require_init();
+// store lifecycle and host-synchronising calls cannot be recorded into a graph
+// (a relaunch would replay freed memory or stale host buffers): they fail
+// while a capture is open
+void require_not_capturing(const char* what);
 Store& store_of(int64_t sid);
 void store_ensure_bytes(Store& s, size_t lo, size_t hi);
 

@@ -620,7 +620,118 @@ __device__ __forceinline__ double dk_add(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ double dk_sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dk_mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dk_div(double a, double b) { return __ddiv_rn(a, b); }
-__device__ __forceinline__ double dk_pow(double a, double b) { return pow(a, b); }
+// ---- '**' (np.power, kernels.py:650) --------------------------------------
+// np.power is libm pow (or SVML on AVX-512 hosts: the two differ by 1 ulp on
+// ~5 % of random inputs, so the reference itself is host-dependent).  CUDA's
+// pow is within 2 ulp.  dk_pow evaluates y*log(x) and exp() in double-double
+// (~2^-100 relative) and rounds once, so its result is the correctly rounded
+// x**y except for subnormal results -- exact whenever x**y is representable
+// (integer data) and within 1 ulp of either host implementation otherwise.
+// Special values follow C99 pow, as numpy does.
+struct dk_dd { double h, l; };
+__device__ __forceinline__ dk_dd dk_dd_fast(double a, double b) { double s = a + b; return {s, b - (s - a)}; }
+__device__ __forceinline__ dk_dd dk_dd_sum(double a, double b) {
+  double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dk_dd dk_dd_add(dk_dd a, dk_dd b) {
+  dk_dd s = dk_dd_sum(a.h, b.h), t = dk_dd_sum(a.l, b.l);
+  s.l = s.l + t.h;
+  s = dk_dd_fast(s.h, s.l);
+  s.l = s.l + t.l;
+  return dk_dd_fast(s.h, s.l);
+}
+__device__ __forceinline__ dk_dd dk_dd_mul(dk_dd a, dk_dd b) {
+  double p = a.h * b.h;
+  double e = __fma_rn(a.h, b.h, -p);
+  e = e + (a.h * b.l + a.l * b.h);
+  return dk_dd_fast(p, e);
+}
+__device__ __forceinline__ dk_dd dk_dd_muld(dk_dd a, double b) {
+  double p = a.h * b;
+  if (!isfinite(p)) return {p, 0.0};
+  double e = __fma_rn(a.h, b, -p) + a.l * b;
+  return dk_dd_fast(p, e);
+}
+__device__ __forceinline__ dk_dd dk_dd_div(dk_dd a, dk_dd b) {
+  double q1 = a.h / b.h;
+  dk_dd r = dk_dd_add(a, dk_dd_muld(b, -q1));
+  double q2 = r.h / b.h;
+  r = dk_dd_add(r, dk_dd_muld(b, -q2));
+  double q3 = r.h / b.h;
+  return dk_dd_add(dk_dd_fast(q1, q2), dk_dd{q3, 0.0});
+}
+__device__ __forceinline__ dk_dd dk_dd_ln2() { return {__longlong_as_double(0x3FE62E42FEFA39EFll), __longlong_as_double(0x3C7ABC9E3B39803Fll)}; }
+// log(x), x > 0 finite: e*ln2 + 2*atanh((m-1)/(m+1)), m in [sqrt(1/2), sqrt(2))
+static __device__ __noinline__ dk_dd dk_dd_log(double x) {
+  int e;
+  double m = frexp(x, &e);
+  if (m < 0.70710678118654752) { m = m * 2.0; e -= 1; }
+  dk_dd s = dk_dd_div(dk_dd{m - 1.0, 0.0}, dk_dd_sum(m, 1.0));  // m - 1 is exact (Sterbenz)
+  dk_dd s2 = dk_dd_mul(s, s);                                      // <= 0.0295
+  dk_dd p = {1.0 / 51.0, 0.0};
+  for (int k = 24; k >= 0; --k) {
+    dk_dd c = k < 12 ? dk_dd_div(dk_dd{1.0, 0.0}, dk_dd{2.0 * k + 1.0, 0.0}) : dk_dd{1.0 / (2.0 * k + 1.0), 0.0};
+    p = dk_dd_add(dk_dd_mul(p, s2), c);
+  }
+  dk_dd lm = dk_dd_mul(s, p);
+  lm.h = lm.h * 2.0;
+  lm.l = lm.l * 2.0;
+  return dk_dd_add(dk_dd_muld(dk_dd_ln2(), (double)e), lm);
+}
+// exp(z) rounded once to double
+static __device__ __noinline__ double dk_dd_exp(dk_dd z) {
+  if (z.h != z.h) return z.h;
+  if (z.h > 709.9) return __longlong_as_double(0x7FF0000000000000ll);
+  if (z.h < -745.3) return 0.0;
+  double kf = rint(z.h * 1.4426950408889634);
+  dk_dd r = dk_dd_add(z, dk_dd_muld(dk_dd_ln2(), -kf));  // |r| <= 0.35
+  r.h = ldexp(r.h, -10);
+  r.l = ldexp(r.l, -10);                                  // |r| < 3.5e-4
+  // e^r - 1 = r (1 + r/2 (1 + r/3 (1 + ... )))
+  dk_dd q = {1.0, 0.0};
+  for (int n = 11; n >= 2; --n) q = dk_dd_add(dk_dd{1.0, 0.0}, dk_dd_div(dk_dd_mul(r, q), dk_dd{(double)n, 0.0}));
+  dk_dd em1 = dk_dd_mul(r, q);
+  for (int i = 0; i < 10; ++i) em1 = dk_dd_mul(em1, dk_dd_add(dk_dd{2.0, 0.0}, em1));  // (1+u)^2 - 1
+  dk_dd v = dk_dd_add(dk_dd{1.0, 0.0}, em1);
+  int k = (int)kf;
+  if (k > 1023) { v.h = v.h * 2.0; v.l = v.l * 2.0; k -= 1; }
+  if (k >= -1021) return ldexp(v.h, k);
+  // subnormal result: round v * 2^k once on the 2^-1074 grid (scaled so the grid
+  // step is 1; both scalings are exact)
+  const double hs = ldexp(v.h, k + 1074), ls = ldexp(v.l, k + 1074);
+  if (hs >= 4503599627370496.0) return ldexp(v.h, k);  // >= 2^-1022: normal after all
+  double g = rint(hs);
+  const double d = (hs - g) + ls;
+  if (d > 0.5 || (d == 0.5 && fmod(g, 2.0) != 0.0)) g = g + 1.0;
+  else if (d < -0.5 || (d == -0.5 && fmod(g, 2.0) != 0.0)) g = g - 1.0;
+  return ldexp(g, -1074);
+}
+static __device__ __noinline__ double dk_pow(double x, double y) {
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+  if (y == 0.0) return 1.0;
+  if (x == 1.0) return 1.0;
+  if (x != x || y != y) return x + y;
+  const double ax = fabs(x);
+  if (isinf(y)) {
+    if (ax == 1.0) return 1.0;
+    return ((ax < 1.0) == (y < 0.0)) ? inf : 0.0;
+  }
+  const bool yint = floor(y) == y;
+  const bool yodd = yint && fabs(y) < 9007199254740992.0 && fmod(y, 2.0) != 0.0;
+  if (x == 0.0) {
+    if (y < 0.0) return yodd ? copysign(inf, x) : inf;
+    return yodd ? x : 0.0;
+  }
+  if (isinf(x)) {
+    if (x > 0.0) return y < 0.0 ? 0.0 : inf;
+    if (y < 0.0) return yodd ? -0.0 : 0.0;
+    return yodd ? -inf : inf;
+  }
+  if (x < 0.0 && !yint) return __longlong_as_double(0x7FF8000000000000ll);
+  const double r = dk_dd_exp(dk_dd_muld(dk_dd_log(ax), y));
+  return (x < 0.0 && yodd) ? -r : r;
+}
 __device__ __forceinline__ bool dk_isnan(double a) { return a != a; }
 __device__ __forceinline__ double dk_min(double a, double b) { return dk_isnan(a) ? a : (a < b ? a : b); }
 __device__ __forceinline__ double dk_max(double a, double b) { return dk_isnan(a) ? a : (a > b ? a : b); }
@@ -1469,7 +1580,25 @@ struct Module {
   std::vector<unsigned int*> ticket;
   std::string src;
   int unroll = 2;
+  // red_part / ticket (and the K3 tile queue) are per-module scratch: two
+  // launches of one module must not overlap.  Launches on one stream are
+  // ordered; when a module moves to another stream the new stream first
+  // waits for everything already enqueued on the previous one.
+  cudaStream_t last_stream = nullptr;
 };
+
+static void order_module(Module* m, cudaStream_t s) {
+  if (m->last_stream && m->last_stream != s && st().capture_launch0 < 0) {
+    static cudaEvent_t ev = [] {
+      cudaEvent_t e = nullptr;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      return e;
+    }();
+    DK_CUDA(cudaEventRecord(ev, m->last_stream));
+    DK_CUDA(cudaStreamWaitEvent(s, ev, 0));
+  }
+  m->last_stream = s;
+}
 
 // A fully prepared launch (parameter blobs, grid shapes) for one exact binding:
 // memo-replayed windows re-launch with identical views and scalars every
@@ -1551,7 +1680,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     if (!plans[n].red_slots.empty() || plans[n].staged) {
       DK_CUDA(cudaMalloc(&rp, sizeof(double) * (size_t)na * (size_t)sms * occ * red_waves() + 64));
       DK_CUDA(cudaMalloc(&tk, sizeof(unsigned int) * 4));
-      DK_CUDA(cudaMemset(tk, 0, sizeof(unsigned int) * 4));
+      DK_CUDA(cudaMemsetAsync(tk, 0, sizeof(unsigned int) * 4, st().stream));
     }
     m->red_part.push_back(rp);
     m->ticket.push_back(tk);
@@ -1595,6 +1724,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   for (size_t i = 0; i < k.recent.size(); ++i) {
     Prepared& pr = k.recent[i];
     if (pr.sig != sig) continue;
+    order_module(pr.m, S.stream);
     for (size_t n = 0; n < pr.blobs.size(); ++n) {
       void* args[] = {pr.blobs[n].data()};
       const unsigned* gd = &pr.grid[4 * n];
@@ -1609,6 +1739,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   Prepared prep;
   prep.sig = sig;
   prep.m = m;
+  order_module(m, S.stream);
   int kbase = 0;
   std::vector<char> blob;
   for (size_t n = 0; n < g.nests.size(); ++n) {
@@ -1837,6 +1968,7 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
                   int point) {
   return guard([&] {
     require_init();
+    require_not_capturing("dk_launch_pub (board slots are epoch-numbered)");
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
     if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);

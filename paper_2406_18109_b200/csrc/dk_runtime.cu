@@ -24,6 +24,8 @@ static State g_state;
 
 State& st() { return g_state; }
 
+void destroy_graphs();  // defined with the graph registry below
+
 void set_last_error(const std::string& msg) { g_err = msg; }
 
 void fail(int code, const char* fmt, ...) {
@@ -37,6 +39,11 @@ void fail(int code, const char* fmt, ...) {
 
 void require_init() {
   if (!g_state.inited) fail(DK_ERR_STATE, "dk_init has not been called");
+}
+
+void require_not_capturing(const char* what) {
+  if (g_state.capture_launch0 >= 0)
+    fail(DK_ERR_STATE, "%s is not allowed while a graph capture is open (it cannot be replayed)", what);
 }
 
 Store& store_of(int64_t sid) {
@@ -311,6 +318,7 @@ namespace dk {
 // Copy the rect [lo, hi) of a store to/from a host array shaped like the whole store.
 static void rect_copy(int64_t sid, const int64_t* lo, const int64_t* hi, void* host, bool up) {
   require_init();
+  require_not_capturing(up ? "dk_store_upload_rect" : "dk_store_download_rect");
   State& S = st();
   Store& s = store_of(sid);
   const int r = s.rank;
@@ -531,26 +539,32 @@ struct GraphRec {
 };
 std::unordered_map<uint64_t, GraphRec> g_graphs;
 uint64_t g_next_graph = 1;
-int64_t g_capture_launch0 = -1;
 }  // namespace
+
+namespace dk {
+void destroy_graphs() {
+  for (auto& kv : g_graphs) cudaGraphExecDestroy(kv.second.exec);
+  g_graphs.clear();
+}
+}  // namespace dk
 
 extern "C" {
 
 int dk_graph_begin(void) {
   return guard([&] {
     require_init();
-    if (g_capture_launch0 >= 0) fail(DK_ERR_ARG, "a graph capture is already open");
+    if (st().capture_launch0 >= 0) fail(DK_ERR_ARG, "a graph capture is already open");
     DK_CUDA(cudaStreamBeginCapture(st().stream, cudaStreamCaptureModeRelaxed));
-    g_capture_launch0 = st().launches;
+    st().capture_launch0 = st().launches;
   });
 }
 
 int dk_graph_end(uint64_t* graph) {
   return guard([&] {
     require_init();
-    if (g_capture_launch0 < 0) fail(DK_ERR_ARG, "no graph capture is open");
-    const int64_t k = st().launches - g_capture_launch0;
-    g_capture_launch0 = -1;
+    if (st().capture_launch0 < 0) fail(DK_ERR_ARG, "no graph capture is open");
+    const int64_t k = st().launches - st().capture_launch0;
+    st().capture_launch0 = -1;
     st().launches -= k;  // captured, not launched
     cudaGraph_t g = nullptr;
     DK_CUDA(cudaStreamEndCapture(st().stream, &g));

@@ -40,6 +40,13 @@ class BoundsError(KernelError):
 
 
 class UnsupportedError(BackendError):
-    """A binding pattern the backend refuses rather than risk wrong results
-    (e.g. a written view overlapping another view of the same store inside
-    one point, which only illegal, non-fused index tasks produce)."""
+    """A binding pattern the backend refuses rather than risk wrong results:
+    overlapping views of one store whose numpy semantics a parallel kernel
+    cannot reproduce (a read after an overlapping write in statement order,
+    overlap inside a per-element nest with offsets; ``aliasing.plan``), or a
+    cross-GPU dependence inside one launch."""
+
+
+class ArenaViolation(BackendError):
+    """ArenaViolationError (executor.py:36-37): under ``isolated`` execution a
+    point writes or reads cells another point of the same launch writes."""

@@ -40,9 +40,10 @@ from typing import Iterable, Mapping, Sequence
 
 import numpy as np
 
+from . import aliasing
 from . import regions as rg
 from . import runtime
-from .errors import BackendError, UnknownTaskKind, UnsupportedError
+from .errors import ArenaViolation, BackendError, UnknownTaskKind, UnsupportedError
 from .initheap import host_contents, poisson_tile, poisson_tile_layout, row_chunks
 from .ir import KProg, TaskDesc, rect_of, slot_access
 from .runtime import DK_F64, DK_I32, check, dk_view, i64s
@@ -116,6 +117,8 @@ class Executor:
         self._scal: dict[tuple, ctypes.Array] = {}
         self._acc: dict[int, tuple] = {}
         self._plans: dict[tuple, tuple] = {}  # launch-plan cache (one GPU)
+        self._alias_c: dict[tuple, tuple] = {}  # (kp, args) -> does a written store have two views
+        self._alias_k: dict[tuple, tuple] = {}  # rewritten kernels of identical-rect alias groups
         self._mplans: dict[tuple, dict] = {}  # launch-plan cache (several GPUs), keyed on coherence state
         self._rec: dict | None = None  # the multi-GPU plan being recorded by execute()
         self.stats = LaunchStats()
@@ -440,11 +443,23 @@ class Executor:
         return a
 
     # ------------------------------------------------------------- execute
-    def execute(self, task: TaskDesc, kp: KProg | None, temp_positions: Iterable[int] = ()) -> None:
-        """Run one (fused or plain) index task: execute_task (executor.py:163-195)."""
+    def execute(self, task: TaskDesc, kp: KProg | None, temp_positions: Iterable[int] = (),
+                isolated: bool = False) -> None:
+        """Run one (fused or plain) index task: execute_task (executor.py:163-195).
+
+        ``isolated``: execute_isolated's contract (executor.py:209-293) -- the
+        per-point write-claim checks (ArenaViolation), then reductions that
+        collect each point's contributions in a zeroed arena before adding it
+        to the target in point order (executor.py:280-293)."""
         if kp is None and task.kind not in BUILTIN_KINDS:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
+        if isolated:
+            if kp is None:
+                raise BackendError(f"isolated execution needs a kernel for kind {task.kind!r}")
+            self.check_isolated(task, temp_positions)
+            self._execute_planned(task, kp, temp_positions, None, isolated=True)
+            return
         use_mplan = os.environ.get("DK_MPLAN", "1") != "0"
         pkey = None
         if kp is not None and self.world == 1:
@@ -616,7 +631,36 @@ class Executor:
         self.stats.points += len(hit["views"])
         self.stats.mplan_hits += 1
 
-    def _execute_planned(self, task: TaskDesc, kp: KProg | None, temp_positions, pkey) -> None:
+    def check_isolated(self, task: TaskDesc, temp_positions) -> None:
+        """execute_isolated's claim checks (executor.py:236-262) on rects: a write
+        overlapping another point's write, or a read / reduction touching cells
+        another point writes, cannot run without communication."""
+        pts = list(task.points())
+        claims: dict[int, list] = {}
+        for o, p in enumerate(pts):
+            for j, a in enumerate(task.args):
+                if j in temp_positions or not a.writes:
+                    continue
+                rect = rect_of(self.shape(a.store), a.part, p)
+                if rg.empty(rect):
+                    continue
+                for o2, r2 in claims.get(a.store, ()):
+                    if o2 != o and rg.overlaps(rect, r2):
+                        raise ArenaViolation(f"write overlap on store {a.store} at point {p} of {task.kind}")
+                claims.setdefault(a.store, []).append((o, rect))
+        for o, p in enumerate(pts):
+            for j, a in enumerate(task.args):
+                if j in temp_positions or a.writes or a.store not in claims:
+                    continue
+                rect = rect_of(self.shape(a.store), a.part, p)
+                if rg.empty(rect):
+                    continue
+                if any(o2 != o and rg.overlaps(rect, r2) for o2, r2 in claims[a.store]):
+                    raise ArenaViolation(
+                        f"point {p} of {task.kind} reads store {a.store} cells written by another point")
+
+    def _execute_planned(self, task: TaskDesc, kp: KProg | None, temp_positions, pkey,
+                         isolated: bool = False) -> None:
         pts = list(task.points())
         V = len(pts)
         prank = [self.point_rank(i, V) for i in range(V)]
@@ -676,7 +720,7 @@ class Executor:
         if kp is None:
             self._run_builtin(task, pts, mine, rects, prank)
         else:
-            recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces)
+            recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces, isolated)
             if recorded is not None and self.world == 1 and pkey is not None:
                 # launch-plan cache: a memo-replayed window over the same
                 # stores re-launches with the bound views as they are
@@ -757,23 +801,60 @@ class Executor:
                             f"{task.kind}: point {i} reads store {sid} written by point {p} on another GPU"
                         )
 
-    def _hazards(self, kp: KProg, task: TaskDesc, rects_p, temp_positions) -> None:
-        params = [(i, s) for i, s in enumerate(kp.slots) if not s.local]
-        wslots = {st[1] for _, _, stmts in kp.nests for st in stmts if st[0] == "store"}
-        for i, s in params:
-            if i not in wslots:
-                continue
-            a = task.args[s.arg]
-            for i2, s2 in params:
-                if i2 == i:
-                    continue
-                b = task.args[s2.arg]
-                if b.store == a.store and rg.overlaps(rects_p[s.arg], rects_p[s2.arg]):
-                    raise UnsupportedError(
-                        f"{task.kind}: written view {s.name} overlaps {s2.name} of the same store {a.store}"
-                    )
+    def _alias_candidates(self, kp: KProg, task: TaskDesc) -> bool:
+        """Does a stored slot share its store with another heap-bound slot?  (cached per binding)"""
+        key = (id(kp), task.args)
+        hit = self._alias_c.get(key)
+        if hit is not None and hit[0] is kp:
+            return hit[1]
+        _, stored, _ = self._access(kp)
+        params = [(i, task.args[s.arg].store) for i, s in enumerate(kp.slots) if not s.local]
+        wstores = {sid for i, sid in params if i in stored}
+        res = len(wstores) > 0 and sum(1 for _, sid in params if sid in wstores) > len(
+            {i for i, sid in params if i in stored})
+        if len(self._alias_c) > 4096:
+            self._alias_c.clear()
+        self._alias_c[key] = (kp, res)
+        return res
 
-    def _run_kernel(self, task, kp, mine, prank, rects, temp_positions, reduces) -> None:
+    def _aliased(self, kp: KProg, task: TaskDesc, rects_p):
+        """Aliasing plan of one point (aliasing.plan): rewritten kernel handle and copy-in slots."""
+        store_of = {i: task.args[s.arg].store for i, s in enumerate(kp.slots) if not s.local}
+        rects = {i: rects_p[kp.slots[i].arg] for i in store_of}
+        mapping, copy_in = aliasing.plan(kp, store_of, rects)
+        h = None
+        if mapping:
+            key = (id(kp), tuple(sorted(mapping.items())))
+            hit = self._alias_k.get(key)
+            if hit is None or hit[0] is not kp:
+                hit = (kp, aliasing.rewrite(kp, mapping))
+                self._alias_k[key] = hit
+            h, _ = self.kernel_handle(hit[1])
+        return h, copy_in
+
+    def _copy_in(self, view: dk_view) -> tuple[dk_view, int]:
+        """Copy a bound view into dense scratch (stream-ordered); returns (scratch view, pointer)."""
+        if view.dtype != DK_F64:
+            raise UnsupportedError("copy-in of an aliased non-f64 view")
+        n = 1
+        for d in range(view.rank):
+            n *= view.ext[d]
+        p = c_uint64()
+        check(self.lib.dk_scratch_alloc(8 * max(n, 1), byref(p)))
+        dst = dk_view()
+        dst.ptr, dst.rank, dst.dtype = p.value, view.rank, DK_F64
+        st_ = 1
+        for d in range(view.rank - 1, -1, -1):
+            dst.ext[d] = view.ext[d]
+            dst.stride[d] = st_
+            st_ *= max(view.ext[d], 1)
+        if n:
+            h, _ = self.kernel_handle(aliasing.copy_kprog(view.rank))
+            pair = (dk_view * 2)(view, dst)
+            check(self.lib.dk_launch(h, pair, 2, self._scalars(()), 0, 0))
+        return dst, p.value
+
+    def _run_kernel(self, task, kp, mine, prank, rects, temp_positions, reduces, isolated=False) -> None:
         if len(kp.scalar_names) != len(task.scalars):
             raise BackendError(
                 f"task {task.kind} carries {len(task.scalars)} scalars, kernel expects {len(kp.scalar_names)}"
@@ -784,7 +865,7 @@ class Executor:
         red_targets = [
             (st[1], kp.slots[st[1]]) for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce"
         ]
-        use_totals = self.world > 1 and nred > 0
+        use_totals = (self.world > 1 or isolated) and nred > 0
         V = len(prank)
         totals = 0
         maxp = 0
@@ -794,7 +875,11 @@ class Executor:
             for q in prank:
                 counts[q] += 1
             maxp = max(counts)
-            if self._p2p and maxp <= runtime.P2P_POINTS and nred <= runtime.P2P_RED:
+            # the board ring is only safe when every rank publishes into every slot
+            # it consumes: a rank without points would only read, so it could fall
+            # DK_P2P_SLOTS epochs behind its peers (their publishes would overwrite
+            # a slot it has not folded yet) -- such launches take the NCCL gather
+            if self._p2p and not isolated and min(counts) >= 1 and maxp <= runtime.P2P_POINTS and nred <= runtime.P2P_RED:
                 pub_slot = self._p2p_epoch % runtime.P2P_SLOTS
                 self._p2p_epoch += 1
                 use_totals = False
@@ -812,10 +897,15 @@ class Executor:
             elif pub_slot >= 0:
                 self._rec["pub"] = True
                 self._rec["counts"] = (c_int32 * self.world)(*counts)
+        aliased = self._alias_candidates(kp, task)
+        if aliased:
+            recorded = None  # copy-ins and rewritten kernels are planned per launch
+            if self._rec is not None:
+                self._rec["ok"] = False
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * nslots)()
             rp = rects[i]
-            self._hazards(kp, task, rp, temp_positions)
+            h_pt, copy_in = self._aliased(kp, task, rp) if aliased else (None, [])
             scratch = []
             for si, s in enumerate(kp.slots):
                 rect = rp[s.arg]
@@ -841,11 +931,15 @@ class Executor:
                     r = self.stores[task.args[s.arg].store]
                     self._ensure(r, rect)
                     views[si] = self.view(r, rect)
+            for si in copy_in:
+                views[si], p = self._copy_in(views[si])
+                scratch.append(p)
+            hl = h if h_pt is None else h_pt
             if pub_slot >= 0:
-                check(self.lib.dk_launch_pub(h, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank))
+                check(self.lib.dk_launch_pub(hl, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank))
             else:
                 tot = totals + 8 * nred * (self.rank * maxp + slot_in_rank) if use_totals else 0
-                check(self.lib.dk_launch(h, views, nslots, scal, len(task.scalars), tot))
+                check(self.lib.dk_launch(hl, views, nslots, scal, len(task.scalars), tot))
             for p in scratch:
                 check(self.lib.dk_scratch_free(p))
             if recorded is not None:
@@ -856,8 +950,14 @@ class Executor:
         if use_totals:
             block = maxp * nred
             gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
-            check(self.lib.dk_comm_allgather_f64(totals + 8 * block * self.rank, gathered, block))
-            self._fold(task, kp, prank, rects, red_targets, gathered, maxp, nred)
+            if self.world > 1:
+                check(self.lib.dk_comm_allgather_f64(totals + 8 * block * self.rank, gathered, block))
+            else:
+                gathered = totals
+            if isolated:
+                self._fold_isolated(task, prank, rects, red_targets, gathered, maxp, nred)
+            else:
+                self._fold(task, kp, prank, rects, red_targets, gathered, maxp, nred)
             check(self.lib.dk_scratch_free(totals))
         elif pub_slot >= 0:
             g = c_uint64()
@@ -915,6 +1015,37 @@ class Executor:
                 tv = self.view(r, rect)
                 self._accum(a.store, tv, gathered, idx[i][k], 1, 1)
 
+    def _fold_isolated(self, task, prank, rects, red_targets, gathered, maxp, nred) -> None:
+        """execute_isolated's combine (executor.py:280-293): per point, a zeroed arena per
+        reduction target collects that target's statements in order, then
+        ``dest += arena`` in point order."""
+        V = len(prank)
+        seen = [0] * self.world
+        arena = c_uint64()
+        check(self.lib.dk_scratch_alloc(8, byref(arena)))
+        av = dk_view()
+        av.ptr, av.rank, av.dtype = arena.value, 0, DK_F64
+        groups: dict[int, list[int]] = {}
+        for k, (sl, _s) in enumerate(red_targets):
+            groups.setdefault(sl, []).append(k)
+        for i in range(V):
+            q = prank[i]
+            base = (q * maxp + seen[q]) * nred
+            seen[q] += 1
+            for sl, ks in groups.items():
+                a = task.args[red_targets[ks[0]][1].arg]
+                if not a.part.is_none and q != self.rank:
+                    continue
+                r = self.stores[a.store]
+                rect = r.full if a.part.is_none else rects[i][red_targets[ks[0]][1].arg]
+                self._ensure(r, rect)
+                check(self.lib.dk_memset_zero(arena.value, 8))
+                for k in ks:
+                    check(self.lib.dk_accum(byref(av), gathered, base + k, 1, 1))
+                tv = self.view(r, rect)
+                check(self.lib.dk_accum(byref(tv), arena.value, 0, 1, 1))
+        check(self.lib.dk_scratch_free(arena.value))
+
     def _run_builtin(self, task, pts, mine, rects, prank) -> None:
         n = len(task.args)
         wflags = (c_int32 * max(n, 1))(*[1 if a.writes else 0 for a in task.args])
@@ -950,7 +1081,21 @@ class Executor:
                 r = self.stores[a.store]
                 self._ensure(r, rects[i][j])
                 views[j] = self.view(r, rects[i][j])
+            # numpy evaluates a builtin's result before assigning it (bufs["a2"][...] = a0 @ a1,
+            # executor.py:93-94): an input overlapping a written argument is read from a copy
+            scratch = []
+            for j, a in enumerate(task.args):
+                if not a.reads or a.writes:
+                    continue
+                if any(b.writes and b.store == a.store and k != j and rg.overlaps(rects[i][j], rects[i][k])
+                       for k, b in enumerate(task.args)):
+                    views[j], p = self._copy_in(views[j])
+                    scratch.append(p)
+            if scratch and self._rec is not None:
+                self._rec["ok"] = False
             check(self.lib.dk_builtin(kind, views, n, wflags))
+            for p in scratch:
+                check(self.lib.dk_scratch_free(p))
             if self._rec is not None:
                 self._rec["views"].append(((views, [(j, a.store) for j, a in enumerate(task.args)]), n, wflags))
         if arenas:

@@ -21,7 +21,7 @@ from typing import Sequence
 
 import numpy as np
 
-from .errors import BoundsError, PrivilegeError, UnknownTaskKind
+from .errors import ArenaViolation, BackendError, BoundsError, PrivilegeError, UnknownTaskKind
 from .executor import BUILTIN_KINDS, Executor
 from .ir import lower_kernel, lower_task
 
@@ -126,12 +126,21 @@ class GpuSession(_RefSession):
                     f"no generator or device builtin for task kind {plan.task.kind!r}"
                 )
             kp = self._lower(kernel, names_fused) if kernel is not None else None
+            # execute_isolated for fused prefixes (pipeline.py:325-334): claim checks and
+            # arena-combined reductions on the device path
+            isolated = plan.f > 1 and self.config.isolated
             try:
-                self.executor.execute(lower_task(plan.task), kp, plan.temp_positions)
+                self.executor.execute(lower_task(plan.task), kp, plan.temp_positions, isolated=isolated)
             except UnknownTaskKind as e:
                 raise _ref_exec.UnknownTaskKindError(str(e)) from e
+            except ArenaViolation as e:
+                raise _ref_exec.ArenaViolationError(str(e)) from e
             except PrivilegeError as e:
                 raise _ref_kernels.PrivilegeViolationError(str(e)) from e
             except BoundsError as e:
                 raise _ref_kernels.OutOfBoundsError(str(e)) from e
+            except BackendError as e:
+                # every other backend failure is the reference's ExecutionError
+                # (executor.py:28-29); the backend type stays on __cause__
+                raise _ref_exec.ExecutionError(f"{type(e).__name__}: {e}") from e
         fr.tasks_out += 1

@@ -40,6 +40,7 @@ class HostStreamer:
         self._events: list[int] = []
         self._last_k = None
         self._last_out = None
+        self._main_ev = None
 
     def _event(self, i: int) -> int:
         while len(self._events) <= i:
@@ -67,6 +68,20 @@ class HostStreamer:
         pts = list(task.points())
         mine = [i for i in range(len(pts)) if ex.point_rank(i, len(pts)) == ex.rank]
         n_ev = 0
+        # everything already enqueued on the executor's main stream (earlier windows
+        # reading these stores, uploads, frees) happens before this window's H2D
+        # and kernels
+        if self._main_ev is None:
+            e = c_uint64()
+            check(lib.dk_event_new(byref(e)))
+            self._main_ev = e.value
+        check(lib.dk_set_stream(self.main))
+        check(lib.dk_event_record(self._main_ev))
+        check(lib.dk_set_stream(s_in))
+        check(lib.dk_stream_wait_event(self._main_ev))
+        check(lib.dk_set_stream(s_k))
+        check(lib.dk_stream_wait_event(self._main_ev))
+        check(lib.dk_set_stream(self.main))
         # WAR across calls: inputs may be overwritten only after the previous kernels,
         # outputs only after the previous D2H
         if self._last_k is not None:

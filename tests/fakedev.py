@@ -95,8 +95,95 @@ def parse_wire(text: str) -> KProg:
     return KProg(tuple(slots), tuple(f"p{i}" for i in range(nscal)), ntemps, tuple(nests), True)
 
 
+def _expr_loads(e):
+    if e[0] == "ld":
+        yield e
+    elif e[0] == "bin":
+        yield from _expr_loads(e[2])
+        yield from _expr_loads(e[3])
+    elif e[0] == "neg":
+        yield from _expr_loads(e[1])
+    elif e[0] == "sel":
+        for x in e[1:]:
+            yield from _expr_loads(x)
+
+
+def _device_interpret(kp, bufs, scal, lshapes, order=1):
+    """What a device kernel observes: elements run one after another (ascending or
+    descending, alternating per launch) with each element's loads hoisted before its
+    stores; a load of a slot this element already stored sees that store (the
+    JIT's same-slot forwarding), a load of any *other* slot sees memory as it was
+    when the element started -- so another slot aliasing the stored memory reads
+    stale data, and a shifted alias reads other elements' new values.
+    Reductions collect per statement and are applied after the nest."""
+    from oracle.interp import _UFUNC
+
+    env = dict(bufs)
+    for i, s in enumerate(kp.slots):
+        if s.local:
+            env[i] = np.zeros(tuple(lshapes[i]), dtype=np.float64)
+    with np.errstate(all="ignore"):
+        for dom, _rank, stmts in kp.nests:
+            bounds = env[dom].shape
+            idxs = list(np.ndindex(*bounds))
+            if order < 0:
+                idxs.reverse()
+            totals = [0.0] * len(stmts)
+            for idx in idxs:
+                def pos(slot, offs):
+                    a = env[slot]
+                    return () if a.ndim == 0 else tuple(i + o for i, o in zip(idx, offs or (0,) * len(idx)))
+                hoist = {}
+                for st in stmts:
+                    e = st[3] if st[0] == "store" else st[2]
+                    for ld in _expr_loads(e):
+                        p = pos(ld[1], ld[2])
+                        a = env[ld[1]]
+                        ok = all(0 <= q < n for q, n in zip(p, a.shape))
+                        hoist[(ld[1], p)] = a[p] if ok else np.nan
+                stored = {}
+                temps = {}
+
+                def ev(e):
+                    t = e[0]
+                    if t == "ld":
+                        p = pos(e[1], e[2])
+                        return stored.get((e[1], p), hoist[(e[1], p)])
+                    if t == "sc":
+                        return np.float64(scal[e[1]])
+                    if t == "c":
+                        return np.float64(e[1])
+                    if t == "t":
+                        return temps[e[1]]
+                    if t == "bin":
+                        return np.float64(_UFUNC[e[1]](ev(e[2]), ev(e[3])))
+                    if t == "neg":
+                        return np.negative(ev(e[1]))
+                    return ev(e[2]) if ev(e[1]) != 0 else ev(e[3])
+
+                for k, st in enumerate(stmts):
+                    if st[0] == "set":
+                        temps[st[1]] = ev(st[2])
+                    elif st[0] == "store":
+                        v = ev(st[3])
+                        p = pos(st[1], st[2])
+                        env[st[1]][p] = v
+                        stored[(st[1], p)] = v
+                    else:
+                        totals[k] = totals[k] + ev(st[2])
+            for k, st in enumerate(stmts):
+                if st[0] == "reduce":
+                    env[st[1]][()] += totals[k]
+
+
 class FakeLib:
-    def __init__(self, rank: int = 0, world: int = 1):
+    def __init__(self, rank: int = 0, world: int = 1, device_model: bool = False):
+        # device_model: every kernel slot reads an independent copy of its view taken
+        # at launch, and stored / reduced slots are written back afterwards -- the
+        # device kernel's view of memory (loads of one slot see that slot's own
+        # stores, never another slot's), so aliased views that the executor does
+        # not rewrite or copy in produce wrong heaps here instead of passing
+        self.device_model = device_model
         self.rank, self.world = rank, world
         self.allocs: dict[int, np.ndarray] = {}  # id -> uint8 buffer
         self.stores: dict[int, tuple] = {}  # sid -> (alloc id, shape, esize)
@@ -255,6 +342,8 @@ class FakeLib:
             out = tb[toff:].view(np.float64)
             for k, arena in enumerate(arenas):
                 out[k] = float(arena.reshape(-1)[0])
+        elif self.device_model:
+            _device_interpret(kp, bufs, scal, lshapes, order=1 if self.launches % 2 == 0 else -1)
         else:
             interpret(kp, bufs, scal, lshapes)
         self.launches += 1
@@ -274,6 +363,12 @@ class FakeLib:
         kind = kind.decode() if isinstance(kind, bytes) else kind
         bufs = [self._view(views[j]) for j in range(n)]
         task = TaskDesc(kind, (1,), tuple(ArgDesc(j, NONE_PART, "W" if writes[j] else "R") for j in range(n)))
+        if self.device_model:
+            # a device builtin streams its inputs while writing: model that as the
+            # inputs observing the written values (wrong unless inputs were copied in)
+            if kind in ("MATVEC", "SPMV") and any(
+                    np.shares_memory(bufs[j], bufs[2]) for j in (0, 1)):
+                bufs[2][...] = np.nan
         default_builtins()[kind](task, bufs)
         self.launches += 1
         return 0

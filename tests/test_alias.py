@@ -1,0 +1,174 @@
+"""Aliased arguments, POW and isolated execution against the reference (CPU).
+
+``tests/golden/alias_streams.json.gz`` holds streams the UNCHANGED reference
+ran (``make_alias_golden.py``): tasks that read and write one store through
+several views, POW tasks, and ``SessionConfig(isolated=True)`` runs, some of
+which the reference rejects with ``ArenaViolationError``.
+
+* the oracle reproduces every heap byte-for-byte (pins the oracle on them);
+* the executor, driven through the CPU stand-in in its *device model* (each
+  kernel slot reads a private copy of its view, as a GPU thread does), must
+  also reproduce them: that only holds if the identical-view rewrite and the
+  copy-ins of ``aliasing.plan`` are right;
+* isolated cases the reference rejects raise ``ArenaViolation`` at the same
+  window.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_arrays, load_golden, same_bits
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return load_golden("alias_streams.json.gz")
+
+
+def test_corpus_shape(cases):
+    names = {c["name"] for c in cases}
+    assert "alias_same_view/unfused" in names and "pow_integer/fused" in names
+    assert sum(1 for c in cases if "error" in c) >= 10
+    assert len(cases) >= 300
+
+
+def test_oracle_matches_reference(cases):
+    from oracle.interp import replay
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    n = 0
+    for c in cases:
+        if "error" in c:
+            continue
+        tr = PlanTrace.from_json(c["trace"])
+        heap = replay(tr)
+        for s, want in golden_arrays(c).items():
+            assert same_bits(heap.get(s), want), (c["name"], s)
+        n += 1
+    assert n > 250
+
+
+def _executor_replay(tr, isolated, device_model=True):
+    from fakedev import FakeLib
+    from paper_2406_18109_b200.executor import Executor
+
+    ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes,
+                  lib=FakeLib(0, 1, device_model=device_model))
+    for kind, ev in tr.events:
+        if kind == "exec":
+            ex.execute(ev.task, ev.kernel, ev.temp_positions, isolated=isolated and ev.f > 1)
+        elif kind == "free":
+            ex.free(ev)
+    return ex
+
+
+def test_executor_device_model_matches_reference(cases):
+    from paper_2406_18109_b200.errors import ArenaViolation
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    checked = raised = 0
+    for c in cases:
+        tr = PlanTrace.from_json(c["trace"])
+        iso = bool(tr.meta.get("isolated"))
+        if "error" in c:
+            with pytest.raises(ArenaViolation):
+                _executor_replay(tr, iso)
+            raised += 1
+            continue
+        ex = _executor_replay(tr, iso)
+        for s, want in golden_arrays(c).items():
+            assert same_bits(ex.get(s), want), (c["name"], s)
+        checked += 1
+    assert checked > 250 and raised >= 10
+
+
+def test_device_model_detects_unhandled_aliasing(cases, monkeypatch):
+    """Without the rewrite / copy-in the device model must produce wrong heaps
+    (so the test above really exercises them)."""
+    from paper_2406_18109_b200 import aliasing
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    monkeypatch.setattr(aliasing, "plan", lambda kp, so, rects: (None, []))
+    wrong = 0
+    for c in cases:
+        if "error" in c or c["name"].endswith("/isolated"):
+            continue
+        tr = PlanTrace.from_json(c["trace"])
+        try:
+            ex = _executor_replay(tr, False)
+        except Exception:  # noqa: BLE001
+            wrong += 1
+            continue
+        if any(not same_bits(ex.get(s), w) for s, w in golden_arrays(c).items()):
+            wrong += 1
+    assert wrong >= 10
+
+
+def test_alias_plan_classification():
+    from paper_2406_18109_b200 import aliasing
+    from paper_2406_18109_b200.errors import UnsupportedError
+    from paper_2406_18109_b200.ir import KProg, Slot
+
+    def kp(stmts, nslots=3):
+        return KProg(tuple(Slot(f"a{i}", i, False, "W" if i == nslots - 1 else "R", 1) for i in range(nslots)), (),
+                     4, ((nslots - 1, 1, tuple(stmts)),), False)
+
+    add = kp([("store", 2, (0,), ("bin", "+", ("ld", 0, (0,)), ("ld", 1, (0,))))])
+    same = {0: ((0,), (4,)), 1: ((0,), (4,)), 2: ((0,), (4,))}
+    m, ci = aliasing.plan(add, {0: 7, 1: 8, 2: 7}, same)
+    assert m == {0: 2} and ci == []
+    shifted = {0: ((0,), (4,)), 1: ((0,), (4,)), 2: ((2,), (6,))}
+    m, ci = aliasing.plan(add, {0: 7, 1: 8, 2: 7}, shifted)
+    assert m is None and ci == [0]
+    disjoint = {0: ((0,), (4,)), 1: ((0,), (4,)), 2: ((4,), (8,))}
+    assert aliasing.plan(add, {0: 7, 1: 8, 2: 7}, disjoint) == (None, [])
+    # a read of the shifted view AFTER the overlapping store: numpy sees the new values
+    late = kp([("store", 2, (0,), ("ld", 1, (0,))), ("store", 2, (0,), ("bin", "+", ("ld", 0, (0,)), ("ld", 2, (0,))))])
+    with pytest.raises(UnsupportedError):
+        aliasing.plan(late, {0: 7, 1: 8, 2: 7}, shifted)
+    # overlap inside a per-element nest with offsets (sequential numpy loop)
+    offs = kp([("store", 2, (0,), ("ld", 0, (1,)))])
+    with pytest.raises(UnsupportedError):
+        aliasing.plan(offs, {0: 7, 1: 8, 2: 7}, shifted)
+
+
+def test_rewrite_preserves_numpy_semantics():
+    """interpret(rewrite(kp)) with private copies per slot == interpret(kp) over aliased views."""
+    from oracle.interp import interpret
+    from paper_2406_18109_b200 import aliasing
+    from paper_2406_18109_b200.ir import KProg, Slot
+
+    slots = (Slot("b0", 0, False, "R", 1), Slot("b1", 1, False, "R", 1), Slot("b2", 2, False, "W", 1),
+             Slot("b3", 3, False, "W", 1))
+    # b2 = b0 + b1 ; b3 = b0 * b2   with b0 and b2 the same view of one store
+    k = KProg(slots, (), 0, ((2, 1, (("store", 2, (0,), ("bin", "+", ("ld", 0, (0,)), ("ld", 1, (0,)))),
+                                     ("store", 3, (0,), ("bin", "*", ("ld", 0, (0,)), ("ld", 2, (0,)))))),), False)
+    x = np.arange(1.0, 9.0)
+    y = np.arange(10.0, 18.0)
+    ref_x, ref_out = x.copy(), np.zeros(8)
+    interpret(k, {0: ref_x, 1: y, 2: ref_x, 3: ref_out}, (), {})
+    m, ci = aliasing.plan(k, {0: 5, 1: 6, 2: 5, 3: 7}, {i: ((0,), (8,)) for i in range(4)})
+    assert m == {0: 2} and not ci
+    k2 = aliasing.rewrite(k, m)
+    dev_x, dev_out = x.copy(), np.zeros(8)
+    copies = {0: np.full(8, np.nan), 1: y.copy(), 2: dev_x, 3: dev_out}  # slot 0 unreferenced now
+    interpret(k2, copies, (), {})
+    assert np.array_equal(dev_x, ref_x) and np.array_equal(dev_out, ref_out)
+
+
+def test_check_isolated_rejects_overlapping_claims():
+    from fakedev import FakeLib
+    from paper_2406_18109_b200.errors import ArenaViolation
+    from paper_2406_18109_b200.executor import Executor
+    from paper_2406_18109_b200.ir import ArgDesc, PartDesc, TaskDesc
+
+    ex = Executor(shapes={0: (10,), 1: (10,)}, lib=FakeLib(0, 1))
+    tile = PartDesc("tiling", (4,), (0,), ((1,),), (0,))
+    wide = PartDesc("tiling", (5,), (0,), ((1,),), (0,))  # 5-wide tiles at stride... tile p -> [5p, 5p+5)
+    shifted = PartDesc("tiling", (4,), (1,), ((1,),), (0,))
+    ok = TaskDesc("COPY", (2,), (ArgDesc(0, tile, "R"), ArgDesc(1, tile, "W")))
+    ex.check_isolated(ok, frozenset())
+    cross_read = TaskDesc("COPY", (2,), (ArgDesc(1, shifted, "R"), ArgDesc(1, tile, "W")))
+    with pytest.raises(ArenaViolation):
+        ex.check_isolated(cross_read, frozenset())
+    ex.check_isolated(TaskDesc("COPY", (2,), (ArgDesc(0, wide, "R"), ArgDesc(1, wide, "W"))), frozenset())

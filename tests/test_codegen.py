@@ -142,3 +142,32 @@ def test_odd_parity_pair_variants(rt, monkeypatch):
     assert "__shfl_down_sync" in b and "dk_st_C(" not in b and "dk_ld_C(" not in b
     b = body(win)  # the window's shifted views (not TMA-staged at this size)
     assert "__shfl_up_sync" in b and "dk_ld_C(" not in b
+
+
+def test_alias_corpus_kernels_compile(rt):
+    """The aliasing / POW / copy-in kernels (alias_streams corpus) compile for sm_100a, incl. dk_pow."""
+    from paper_2406_18109_b200 import aliasing
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    seen = set()
+    n_pow = 0
+    for case in load_golden("alias_streams.json.gz"):
+        tr = PlanTrace.from_json(case["trace"])
+        for e in tr.execs():
+            if e.kernel is None or e.kernel.wire([s.decl_rank for s in e.kernel.slots]) in seen:
+                continue
+            seen.add(e.kernel.wire([s.decl_rank for s in e.kernel.slots]))
+            src = codegen(rt, e.kernel, views_for(rt, e.task, e.kernel, tr.shapes))
+            n_pow += "dk_pow(" in src.split("__global__", 1)[-1]
+    for r in (1, 2):
+        kp = aliasing.copy_kprog(r)
+        codegen(rt, kp, views_for(rt, _copy_task(r), kp, {0: (6,) * r, 1: (6,) * r}))
+    assert n_pow >= 2
+
+
+def _copy_task(rank):
+    from paper_2406_18109_b200.ir import ArgDesc, PartDesc, TaskDesc
+
+    ident = tuple(tuple(1 if i == j else 0 for j in range(rank)) for i in range(rank))
+    p = PartDesc("tiling", (6,) * rank, (0,) * rank, ident, (0,) * rank)
+    return TaskDesc("COPY", (1,) * rank, (ArgDesc(0, p, "R"), ArgDesc(1, p, "W")))
