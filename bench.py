@@ -216,6 +216,177 @@ def reference_session_rate(size, budget_s=None, warmup=3, steps=None):
     return n / dt, n, dt
 
 
+def fresh_targets(ex, trace, events):
+    """Free rank-0 reduction targets an earlier replay of these recorded events left behind.
+
+    The recorded plans hold 24 iterations; longer runs cycle through the steady
+    ones.  Each iteration creates its own reduction targets (pq, rs_old, rs_new,
+    res), zero-initialised (``initheap``); a cycled iteration would find them
+    still holding last cycle's value and accumulate onto it.  Freeing them first
+    keeps every replayed iteration the stream the front end recorded."""
+    for k, e in events:
+        if k == "exec":
+            for a in e.task.args:
+                if a.reduces and trace.shapes.get(a.store) == () and a.store in ex.stores:
+                    ex.free(a.store)
+
+
+def _rows_parallel(fn, n, workers=None):
+    """fn(r0, r1) over row chunks of [0, n) on a thread pool (numpy releases the GIL); results in order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    workers = workers or min(16, os.cpu_count() or 1)
+    step = max(1, -(-n // (4 * workers)))
+    with ThreadPoolExecutor(workers) as pool:
+        return list(pool.map(lambda r: fn(r, min(n, r + step)), range(0, n, step)))
+
+
+def _allsum(torch, world, x):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def result_check(ex, trace, wl, its, nxt, torch, world):
+    """Check one more iteration of a full-size run (outside the timed region) by the
+    workload's own identities -- no oracle: every rank checks its own band.
+
+    * stencil: work == 0.2 * ((((c + n) + e) + w) + s) bit for bit from the grid before
+      the sweep (band-interior rows), grid centre == work after the COPY, and
+      res == sum((work - c)^2) within rtol 1e-12 (N = 1: needs every row);
+    * cg / pcg: resid == -r (cg tail), z == 0.25 * r (pcg), rs_new / rz_new == r.r / r.z
+      within rtol 1e-12 (host partials summed over ranks), and the recurrence residual
+      matches the true one: ||b - A x - r|| <= 1e-9 ||b|| (A applied on band-interior rows)."""
+    import numpy as np
+
+    from paper_2406_18109_b200.executor import replay
+
+    events = its[nxt]
+    fresh_targets(ex, trace, events)
+    execs = [e for k, e in events if k == "exec"]
+    pt = [i for i in range(execs[0].task.volume) if ex.point_rank(i, execs[0].task.volume) == ex.rank]
+    out = {}
+    if wl == "stencil":
+        grid, work = 0, 1
+        H, Wd = trace.shapes[grid]
+        n = Wd - 2
+        band = (H - 2) // max(1, execs[0].task.volume)
+        lo, hi = pt[0] * band, (pt[-1] + 1) * band  # interior rows of this rank (work coordinates)
+        g0 = np.empty(trace.shapes[grid])
+        ex.download_local(grid, g0, ((lo + 1, 0), (hi + 1, Wd)))  # this rank's rows (neighbours' halo rows are stale)
+        if lo == 0:  # border rows: only their interior columns are ever read (the corners never are)
+            ex.download_local(grid, g0, ((0, 1), (1, Wd - 1)))
+        if hi == H - 2:
+            ex.download_local(grid, g0, ((H - 1, 1), (H, Wd - 1)))
+        replay(ex, events)
+        ex.sync()
+        red = [a.store for e in execs for a in e.task.args if a.reduces and trace.shapes[a.store] == ()]
+        w = np.empty(trace.shapes[work])
+        ex.download_local(work, w, ((lo, 0), (hi, n)))
+        g1 = np.empty(trace.shapes[grid])
+        ex.download_local(grid, g1, ((lo + 1, 0), (hi + 1, Wd)))
+        # rows whose four neighbours this rank held before the sweep: all of them at N = 1
+        a = lo + (1 if lo > 0 else 0)
+        b = hi - (1 if hi < H - 2 else 0)
+
+        def sweep(r0, r1):
+            r0, r1 = r0 + a, r1 + a
+            c = g0[r0 + 1:r1 + 1, 1:-1]
+            want = ((((c + g0[r0:r1, 1:-1]) + g0[r0 + 1:r1 + 1, 2:]) + g0[r0 + 1:r1 + 1, :-2]) + g0[r0 + 2:r1 + 2, 1:-1]) * 0.2
+            ok = want.tobytes() == w[r0:r1].tobytes()
+            d = w[r0:r1] - c
+            return ok, float(np.sum(d * d))
+
+        parts = _rows_parallel(sweep, b - a)
+        ok_work = all(p[0] for p in parts)
+        ok_copy = g1[lo + 1:hi + 1, 1:-1].tobytes() == w[lo:hi].tobytes()
+        out["work_bit_identical"] = ok_work
+        out["copy_bit_identical"] = ok_copy
+        ok = ok_work and ok_copy
+        if world == 1:
+            tot = 0.0
+            for p in parts:
+                tot += p[1]
+            res = float(ex.get(red[-1])[()])
+            out["res_rel_err"] = abs(res - tot) / tot
+            ok = ok and out["res_rel_err"] <= 1e-12
+    elif wl == "bs":
+        replay(ex, events)
+        ex.sync()
+        t = execs[0].task
+        xs, ys = t.args[0].store, t.args[1].store
+        outs = [a.store for e in execs for a in e.task.args if a.priv == "W" and a.store in trace.live][-1]
+        n = trace.shapes[xs][0] // t.volume
+        rect = ((pt[0] * n,), ((pt[-1] + 1) * n,))
+        v = [ex.download_local(sid, np.empty(trace.shapes[sid]), rect)[rect[0][0]:rect[1][0]] for sid in (xs, ys, outs)]
+        ok = v[2].tobytes() == (v[0] + v[1]).tobytes()
+        out["out_eq_x_plus_y"] = ok  # the chain's operator cycle is the identity (trace.py:280-285)
+    else:
+        n = trace.shapes[3][0]
+        init = trace.init
+        nx, ny = int(init[1]["nx"]), int(init[1]["ny"])
+        x_sid, r_sid = 3, 4
+        assert init[x_sid]["kind"] == "zeros" and init[r_sid]["kind"] == "uniform" and "scale" not in init[r_sid]
+        replay(ex, events)
+        ex.sync()
+        t = n // execs[0].task.volume
+        lo, hi = pt[0] * t, (pt[-1] + 1) * t
+        rect = ((lo,), (hi,))
+        vec = {}
+        for name, sid in (("x", x_sid), ("r", r_sid), ("aux", 7 if wl == "cg" else 6)):
+            vec[name] = ex.download_local(sid, np.empty(trace.shapes[sid]), rect)[lo:hi]
+        red_win = [e for e in execs if any(a.store == r_sid and a.writes for a in e.task.args)]
+        tgt = [a.store for a in red_win[-1].task.args if a.reduces and trace.shapes[a.store] == ()][-1]
+        if wl == "cg":
+            out["resid_eq_minus_r"] = bool(np.array_equal(vec["aux"], -vec["r"]))
+            dot = _allsum(torch, world, sum(_rows_parallel(lambda a, b: float(np.dot(vec["r"][a:b], vec["r"][a:b])), hi - lo)))
+            ok = out["resid_eq_minus_r"]
+        else:
+            zz = 0.25 * vec["r"]
+            out["z_bits_eq_r_quarter"] = zz.tobytes() == vec["aux"].tobytes()
+            dot = _allsum(torch, world, sum(_rows_parallel(lambda a, b: float(np.dot(vec["r"][a:b], vec["aux"][a:b])), hi - lo)))
+            ok = out["z_bits_eq_r_quarter"]
+        got = float(ex.get(tgt)[()]) if world == 1 else float(ex.download_local(tgt, np.empty(()), ((), ()))[()])
+        out["dot_rel_err"] = abs(got - dot) / abs(dot)
+        ok = ok and out["dot_rel_err"] <= 1e-12
+        # true residual b - A x vs the recurrence's r (A = 5-point Laplacian, grid rows of nx)
+        b = np.random.default_rng([int(init[r_sid].get("seed", 0)), int(init[r_sid]["key"])]).random(n)[lo:hi]
+        X = vec["x"].reshape(-1, nx)
+        R = vec["r"].reshape(-1, nx)
+        B = b.reshape(-1, nx)
+        g_lo, g_hi = lo // nx, hi // nx
+        ra = 1 if g_lo > 0 else 0
+        rb = X.shape[0] - (1 if g_hi < ny else 0)
+
+        def resid(a, c):
+            a, c = a + ra, c + ra
+            ax = 4.0 * X[a:c]
+            ax[:, 1:] -= X[a:c, :-1]
+            ax[:, :-1] -= X[a:c, 1:]
+            if a > 0:
+                ax -= X[a - 1:c - 1]
+            else:
+                ax[1:] -= X[a:c - 1]
+            if c < X.shape[0]:
+                ax -= X[a + 1:c + 1]
+            else:
+                ax[:-1] -= X[a + 1:c]
+            d = B[a:c] - ax - R[a:c]
+            return float(np.sum(d * d)), float(np.sum(B[a:c] * B[a:c]))
+
+        parts = _rows_parallel(resid, rb - ra)
+        num = _allsum(torch, world, sum(p[0] for p in parts))
+        den = _allsum(torch, world, sum(p[1] for p in parts))
+        out["true_residual_gap"] = (num / den) ** 0.5
+        ok = ok and out["true_residual_gap"] <= 1e-9
+    out["status"] = "ok" if ok else "FAILED"
+    return out
+
+
 def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True, sync_ranks=None):
     """Warm-up W iterations past the ramp, then time exactly K iterations on the executor's stream,
     bracketed by ``sync_ranks`` (barrier + device synchronize on every rank) on both sides."""
@@ -224,7 +395,10 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
 
     its, steady = iteration_split(trace)
     seq = list(range(steady)) + [steady + (i % (len(its) - steady)) for i in range(warmup + steps)]
+    cycled = len(seq) > len(its)
     for i in seq[: steady + warmup]:
+        if cycled:
+            fresh_targets(ex, trace, its[i])
         replay(ex, its[i])
     ex.sync()
     if sync_ranks is not None:
@@ -241,6 +415,8 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
     start.record(ext_stream)
     th0 = time.perf_counter()
     for i in timed:
+        if cycled:
+            fresh_targets(ex, trace, its[i])  # host-side frees of 8-byte stores (only when cycling)
         for k, e in its[i]:
             if k == "exec":
                 if with_events:
@@ -283,6 +459,7 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
         if k == "exec":
             mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
             it_bytes += launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
+    measure.next_iteration = steady + ((warmup + steps) % (len(its) - steady))
     return ms, launches, dom, it_bytes
 
 
@@ -533,12 +710,20 @@ def run_ours(args):
                                                   sync_ranks=sync_ranks)
             if sampler:
                 sampler.mark("t1")
+            check = None
+            if plan is None and not args.no_check:
+                # one more iteration, outside the timed region, checked by the workload's identities
+                try:
+                    its, _ = iteration_split(trace)
+                    check = result_check(ex, trace, wl, its, measure.next_iteration, torch, world)
+                except Exception as exc:  # noqa: BLE001
+                    check = {"status": "FAILED", "error": f"{type(exc).__name__}: {exc}"}
             per_rank = gather_all(torch, world, ms / (steps or args.steps))
             host_rank = gather_all(torch, world, measure.host_ms / (steps or args.steps))
             ms = reduce_max(torch, world, ms)
             res = {"ms": ms, "ranks_ms_per_step": per_rank, "host_ms_per_step": host_rank, "launches": launches,
                    "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats),
-                   "jit": ex.jit_stats()}
+                   "jit": ex.jit_stats(), "check": check}
             if with_e2e:
                 e_ms, bi, bo, ok = e2e_bs(ex, trace, args.steps, torch, ext, world)
                 res["e2e"] = (reduce_max(torch, world, e_ms), bi, bo, ok)
@@ -605,6 +790,7 @@ def run_ours(args):
         "host_enqueue_ms_per_step": main["host_ms_per_step"],
         "jit": main["jit"],
         "clocks": clocks,
+        "result_check": main["check"],
     }
     if "e2e" in main:
         e_ms, bi, bo, ok = main["e2e"]
@@ -616,7 +802,7 @@ def run_ours(args):
         try:
             un = one(wl, "unfused")
             out["unfused"] = {"value": round(world * K / (un["ms"] / 1e3), 4), "ms_per_step": round(un["ms"] / K, 3),
-                              "gpu_launches": un["launches"]}
+                              "gpu_launches": un["launches"], "result_check": un["check"]}
             out["fused_over_unfused"] = round(un["ms"] / main["ms"], 3)
         except Exception as exc:  # noqa: BLE001
             out["unfused"] = {"error": f"{type(exc).__name__}: {exc}"}
@@ -637,6 +823,8 @@ def run_ours(args):
                     "fused_hbm_frac_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9 / hbm_peak, 4),
                     "dominant": {"kind": d["kind"], "f": d["f"], "avg_ms": round(d["avg_ms"], 4),
                                  "gbs": round(d["bytes"] / (d["avg_ms"] / 1e3) / 1e9, 1)} if d else None,
+                    "result_check": f["check"],
+                    "unfused_result_check": u["check"],
                 }
             except Exception as exc:  # noqa: BLE001
                 others[w2] = {"error": f"{type(exc).__name__}: {exc}"}
@@ -740,6 +928,7 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--quick", action="store_true", help="headline device timing only (no e2e, extras, CPU baseline)")
     ap.add_argument("--pre", default="", help="diagnostics: workloads to run in this process before the timed one")
+    ap.add_argument("--no-check", action="store_true", help="skip the post-run result checks")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -25,10 +25,24 @@ Parity pinning: ``tests/golden/make_golden.py`` runs the unchanged reference
 on benchmark traces and a fuzz corpus and stores its final heap digests;
 ``tests/test_oracle_golden.py`` replays the recorded plans through this
 oracle and requires byte-identical heaps.
+
+Full-size runs (``replay(..., workers=N)``, BASELINE sizes: 32768^2 grids,
+67M-row CG) split zero-offset nests into row chunks evaluated on N threads
+(numpy releases the GIL) and run ``SPMV_CSR`` through the C restatement in
+``oracle/csrc/spmv_csr.c``.  Every stored value is computed by exactly the same
+element-wise operations as the whole-array path (a nest is only chunked when
+no written view aliases another view and every bound array has the nest's
+shape); only reductions change: each chunk is summed with ``np.sum`` and the
+chunk sums are added in order, a different summation order from one
+``np.sum`` (the device's order differs as well, so reductions are compared
+at rtol).  ``tests/test_oracle_golden.py`` pins the chunked mode too.
 """
 
 from __future__ import annotations
 
+import ctypes
+import os
+from concurrent.futures import ThreadPoolExecutor
 from typing import Callable, Mapping, Sequence
 
 import numpy as np
@@ -265,9 +279,45 @@ def spmv_csr_rows(rowptr: np.ndarray, cols: np.ndarray, vals: np.ndarray, x: np.
     return acc
 
 
+_CLIB = None
+
+
+def _clib():
+    """oracle/liboracle.so (built by oracle/build.py), or None."""
+    global _CLIB
+    if _CLIB is None:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liboracle.so")
+        if not os.path.exists(path):
+            _CLIB = False
+        else:
+            lib = ctypes.CDLL(path)
+            f = lib.oracle_spmv_csr_f64idx
+            f.restype = None
+            f.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int]
+            _CLIB = lib
+    return _CLIB or None
+
+
+def spmv_csr_rows_c(rowptr, cols, vals, x, nthreads: int) -> np.ndarray:
+    """spmv_csr_rows through the C restatement (same per-row order and roundings)."""
+    lib = _clib()
+    if lib is None:
+        raise OracleError("oracle/liboracle.so is not built (python oracle/build.py)")
+    arrs = [np.ascontiguousarray(a.reshape(-1), dtype=np.float64) for a in (rowptr, cols, vals, x)]
+    nrows = arrs[0].size - 1
+    y = np.empty(max(nrows, 0), dtype=np.float64)
+    if nrows > 0:
+        lib.oracle_spmv_csr_f64idx(*(a.ctypes.data for a in arrs), y.ctypes.data, nrows, int(nthreads))
+    return y
+
+
 def _spmv_csr(task: TaskDesc, bufs: list) -> None:
     # args: rowptr (1, t+1) R, cols (1, nnz) R, vals (1, nnz) R, x (NonePart) R, y (t,) W
-    bufs[4][...] = spmv_csr_rows(bufs[0], bufs[1], bufs[2], bufs[3]).reshape(bufs[4].shape)
+    if _WORKERS > 1 and bufs[4].size >= (1 << 16) and _clib() is not None:
+        y = spmv_csr_rows_c(bufs[0], bufs[1], bufs[2], bufs[3], _WORKERS)
+    else:
+        y = spmv_csr_rows(bufs[0], bufs[1], bufs[2], bufs[3])
+    bufs[4][...] = y.reshape(bufs[4].shape)
 
 
 def default_builtins() -> dict[str, Builtin]:
@@ -284,6 +334,95 @@ def _view(a: np.ndarray, rect) -> np.ndarray:
     if not lo:
         return a
     return a[tuple(slice(l, h) for l, h in zip(lo, hi))]
+
+
+_WORKERS = 1
+_CHUNK_ELEMS = 1 << 22
+
+
+def _same_view(a: np.ndarray, b: np.ndarray) -> bool:
+    ia, ib = a.__array_interface__, b.__array_interface__
+    return ia["data"][0] == ib["data"][0] and a.shape == b.shape and a.strides == b.strides
+
+
+def _nest_chunkable(kp: KProg, nest, bufs: Mapping[int, np.ndarray]) -> bool:
+    dom, _rank, stmts = nest
+    if not _zero_offsets(stmts) or dom not in bufs:
+        return False
+    shape = bufs[dom].shape
+    if len(shape) == 0 or shape[0] < 2:
+        return False
+    used, stored, reduced, loaded0 = set(), set(), set(), set()
+    for st in stmts:
+        e = st[3] if st[0] == "store" else st[2]
+        for ld in _loads(e):
+            used.add(ld[1])
+            if bufs.get(ld[1]) is not None and bufs[ld[1]].ndim == 0:
+                loaded0.add(ld[1])
+        if st[0] == "store":
+            stored.add(st[1])
+            used.add(st[1])
+        elif st[0] == "reduce":
+            reduced.add(st[1])
+    for i in used:
+        if i not in bufs:
+            return False  # a task-local buffer
+        if bufs[i].ndim and bufs[i].shape != shape:
+            return False  # broadcasting between ranks: keep the whole-array path
+    for i in reduced:
+        if i not in bufs or bufs[i].ndim != 0 or i in loaded0 or i in stored:
+            return False
+        if any(np.may_share_memory(bufs[i], bufs[j]) for j in used):
+            return False
+    for w in stored:
+        for j in used:
+            if j != w and np.may_share_memory(bufs[w], bufs[j]) and not _same_view(bufs[w], bufs[j]):
+                return False
+    return True
+
+
+def _interpret_chunked(kp: KProg, bufs: dict, scalars, pool: ThreadPoolExecutor) -> None:
+    """``interpret`` for kernels without locals, nest by nest, row chunks on ``pool``."""
+    for nest in kp.nests:
+        dom, rank, stmts = nest
+        if not _nest_chunkable(kp, nest, bufs):
+            one = KProg(kp.slots, kp.scalar_names, kp.ntemps, (nest,), kp.fused_names)
+            interpret(one, bufs, scalars, {})
+            continue
+        n0 = bufs[dom].shape[0]
+        inner = int(np.prod(bufs[dom].shape[1:])) if bufs[dom].ndim > 1 else 1
+        rows = max(1, min(_CHUNK_ELEMS // max(inner, 1), -(-n0 // (4 * _WORKERS))))
+        bounds = [(r, min(n0, r + rows)) for r in range(0, n0, rows)]
+        red = [k for k, st in enumerate(stmts) if st[0] == "reduce"]
+        # each reduce statement gets a private 0-d arena per chunk
+        slots = list(kp.slots)
+        new_stmts = []
+        arena_of = {}
+        for k, st in enumerate(stmts):
+            if st[0] == "reduce":
+                arena_of[k] = len(slots)
+                from paper_2406_18109_b200.ir import Slot
+
+                slots.append(Slot(f"rd{k}", -1, False, "Rd", 0))
+                new_stmts.append(("reduce", arena_of[k], st[2]))
+            else:
+                new_stmts.append(st)
+        kc = KProg(tuple(slots), kp.scalar_names, kp.ntemps, ((dom, rank, tuple(new_stmts)),), kp.fused_names)
+
+        def run(b, kc=kc):
+            r0, r1 = b
+            sub = {i: (a[r0:r1] if a.ndim else a) for i, a in bufs.items()}
+            arenas = {arena_of[k]: np.zeros(()) for k in red}
+            sub.update(arenas)
+            interpret(kc, sub, scalars, {})
+            return [float(arenas[arena_of[k]][()]) for k in red]
+
+        parts = list(pool.map(run, bounds))
+        for idx, k in enumerate(red):
+            total = 0.0
+            for p in parts:
+                total = total + p[idx]
+            bufs[stmts[k][1]][()] += total
 
 
 def execute_step(step: ExecStep, heap: OracleHeap, builtins: Mapping[str, Builtin] | None = None) -> None:
@@ -311,14 +450,44 @@ def execute_step(step: ExecStep, heap: OracleHeap, builtins: Mapping[str, Builti
                 lshapes[i] = tuple(max(0, h - l) for l, h in zip(*r))
             else:
                 bufs[i] = _view(heap.get(a.store), r)
-        interpret(kp, bufs, task.scalars, lshapes)
+        if _POOL is not None and not lshapes:
+            _interpret_chunked(kp, bufs, task.scalars, _POOL)
+        else:
+            interpret(kp, bufs, task.scalars, lshapes)
 
 
-def replay(trace: PlanTrace, events=None, heap: OracleHeap | None = None, builtins=None) -> OracleHeap:
+_POOL: ThreadPoolExecutor | None = None
+
+
+class parallel:
+    """``with parallel(n):`` -- chunked, threaded evaluation (full-size parity runs)."""
+
+    def __init__(self, workers: int | None = None) -> None:
+        self.workers = workers or os.cpu_count() or 1
+
+    def __enter__(self):
+        global _POOL, _WORKERS
+        self._saved = (_POOL, _WORKERS)
+        if self.workers > 1:
+            _WORKERS = self.workers
+            _POOL = ThreadPoolExecutor(self.workers)
+        return self
+
+    def __exit__(self, *exc):
+        global _POOL, _WORKERS
+        if _POOL is not None and _POOL is not self._saved[0]:
+            _POOL.shutdown()
+        _POOL, _WORKERS = self._saved
+        return False
+
+
+def replay(trace: PlanTrace, events=None, heap: OracleHeap | None = None, builtins=None,
+           workers: int = 1) -> OracleHeap:
     heap = heap or OracleHeap(trace.shapes, trace.seed, trace.init)
-    for kind, ev in (events if events is not None else trace.events):
-        if kind == "exec":
-            execute_step(ev, heap, builtins)
-        elif kind == "free":
-            heap.free(ev)
+    with parallel(workers):
+        for kind, ev in (events if events is not None else trace.events):
+            if kind == "exec":
+                execute_step(ev, heap, builtins)
+            elif kind == "free":
+                heap.free(ev)
     return heap

@@ -65,3 +65,51 @@ def test_heap_default_contents_rule():
     assert a.dtype == np.float64 and a.min() >= 1 and a.max() <= 9
     h.free(0)
     assert (h.get(0) == a).all()
+
+
+def _integer_valued(arrs):
+    return all(np.all(np.isfinite(a)) and np.all(a == np.round(a)) for a in arrs.values())
+
+
+def test_chunked_parallel_mode_matches_reference(bench_cases, fuzz_cases, monkeypatch):
+    """The full-size mode (row chunks on threads, C SPMV_CSR) reproduces the reference's heaps:
+    bit-exact on integer data (every sum exact in any order), rtol 1e-12 on the real-valued CG
+    plans (chunk sums are added in a different order than one np.sum)."""
+    import oracle.interp as oi
+
+    monkeypatch.setattr(oi, "_CHUNK_ELEMS", 7)  # force many chunks on the small golden stores
+    calls = []
+    orig = oi._interpret_chunked
+
+    def spy(*a, **k):
+        calls.append(1)
+        return orig(*a, **k)
+
+    monkeypatch.setattr(oi, "_interpret_chunked", spy)
+    n_exact = n_chunked = 0
+    for case in list(bench_cases) + list(fuzz_cases)[::5]:
+        trace = PlanTrace.from_json(case["trace"])
+        calls.clear()
+        heap = replay(trace, workers=4)
+        n_chunked += bool(calls)
+        gold = golden_arrays(case)
+        if _integer_valued(gold):
+            n_exact += 1
+            assert all(same_bits(heap.get(s), g) for s, g in gold.items()), case["name"]
+        else:
+            for s, g in gold.items():
+                np.testing.assert_allclose(heap.get(s), g, rtol=1e-12, atol=1e-12 * float(np.max(np.abs(g))),
+                                           err_msg=case["name"])
+    assert n_exact > 100 and n_chunked > 50
+
+
+def test_c_spmv_matches_numpy_restatement():
+    from oracle.interp import spmv_csr_rows_c
+
+    rng = np.random.default_rng(3)
+    for nx, ny, k in ((7, 9, 1), (64, 64, 2), (33, 40, 4)):
+        for p in range(k):
+            rp, cl, vl = poisson_tile(nx, ny, k, p)
+            vl = vl * rng.random(vl.size)
+            x = rng.random(nx * ny) - 0.5
+            assert same_bits(spmv_csr_rows_c(rp, cl, vl, x, 4), spmv_csr_rows(rp, cl, vl, x))

@@ -52,9 +52,26 @@ def capture(name, gen, iters, fused, execute=False):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--large-only" in sys.argv:
+        large()
+        return
     if "--medium-only" not in sys.argv:
         full_size()
     medium()
+    large()
+
+
+def large():
+    """Multi-band plans at large size for the one-GPU full-size parity tests (tests/test_gpu_fullsize.py):
+    four 8192^2 bands on one GPU (four launch points per launch)."""
+    out = []
+    for fused in (True, False):
+        tr = capture(f"stencil_8192_k4/{'fused' if fused else 'unfused'}", lambda it: W.stencil_bands(8192, 4, it),
+                     12 if fused else 6, fused)
+        out.append(tr.to_json())
+    with gzip.open(os.path.join(REPO, "tests", "golden", "plans_large.json.gz"), "wt", compresslevel=9) as f:
+        json.dump({"format": "dk-plans-1", "traces": out}, f, separators=(",", ":"))
+    print("large traces:", len(out))
 
 
 def full_size():
