@@ -98,6 +98,176 @@ __global__ void __launch_bounds__(256) k_spmv_csr(const I* __restrict__ rowptr, 
   }
 }
 
+// ---- SPMV_CSR, bulk-copy pipeline (int32 indices) ----------------------------
+// Persistent CTAs of 8 consumer warps + 1 producer warp.  The matrix is cut
+// into chunks of kSpR rows; chunk c's rowptr slab and its contiguous nonzero
+// slab [rowptr[r0], rowptr[r1]) of vals and cols are moved into a shared-memory
+// stage by three cp.async.bulk copies (16-byte-rounded ranges: rounding never
+// leaves the 2 MiB granule a view lies in) completing on the stage's full
+// mbarrier; consumers release the stage on its empty mbarrier.  kSpStages
+// stages keep ~100 KB per CTA in flight, so the nonzero stream no longer
+// waits on per-thread dependent loads.  Each consumer thread then sums one
+// row from shared memory: acc = 0.0; acc = acc + vals[j] * x[cols[j]] left
+// to right with __dmul_rn / __dadd_rn -- the same order and roundings as the
+// oracle's definition, so the result is bit-identical to k_spmv_csr.  A chunk
+// whose nonzeros exceed the stage capacity is flagged and read from global.
+// Optional epilogue (dot != nullptr): per-CTA partial of sum_i p[i] * y[i]
+// over the tile's rows (p = x at row offset x_row0), for the opt-in SpMV +
+// partial-dot fusion; per-thread in row order, then a fixed warp / CTA tree.
+namespace {
+constexpr int kSpR = 256;
+constexpr int kSpCap = 2048;
+constexpr int kSpStages = 4;
+constexpr int kSpConsumers = kSpR / 32;
+struct __align__(16) SpStage {
+  double vals[kSpCap + 2];
+  int32_t cols[kSpCap + 4];
+  int32_t rowptr[kSpR + 8];
+  int64_t rp0;
+  int32_t voff, coff, roff, mode;
+};
+struct SpShared {
+  SpStage st[kSpStages];
+  unsigned long long full[kSpStages], empty[kSpStages];
+  double red[kSpConsumers];
+};
+__device__ __forceinline__ uint32_t sp_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void sp_wait(uint32_t bar, uint32_t ph) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(bar), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void sp_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kSpR + 32, 2)
+    k_spmv_csr_bulk(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                    const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y,
+                    int64_t nrows, double* __restrict__ dot, int64_t x_row0) {
+  extern __shared__ __align__(16) unsigned char sp_raw[];
+  SpShared& S = *reinterpret_cast<SpShared*>(sp_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nchunks = (nrows + kSpR - 1) / kSpR;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSpStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&S.full[s])), "r"(1) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&S.empty[s])), "r"(kSpConsumers) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kSpConsumers) {  // producer
+    if (lane == 0) {
+      int64_t c = blockIdx.x;
+      int64_t nr0 = 0, nr1 = 0;
+      if (c < nchunks) {
+        nr0 = __ldg(rowptr + c * kSpR);
+        nr1 = __ldg(rowptr + (c * kSpR + kSpR < nrows ? c * kSpR + kSpR : nrows));
+      }
+      for (int64_t k = 0; c < nchunks; c += gridDim.x, ++k) {
+        const int s = (int)(k % kSpStages);
+        if (k >= kSpStages) sp_wait(sp_smem(&S.empty[s]), (uint32_t)(((k / kSpStages) - 1) & 1));
+        const int64_t r0 = c * kSpR, r1 = (r0 + kSpR < nrows ? r0 + kSpR : nrows);
+        const int64_t rp0 = nr0, rp1 = nr1;
+        // prefetch the next chunk's boundaries (consumed one iteration later)
+        const int64_t cn = c + gridDim.x;
+        if (cn < nchunks) {
+          nr0 = __ldg(rowptr + cn * kSpR);
+          nr1 = __ldg(rowptr + (cn * kSpR + kSpR < nrows ? cn * kSpR + kSpR : nrows));
+        }
+        SpStage& st = S.st[s];
+        st.rp0 = rp0;
+        const uint32_t fb = sp_smem(&S.full[s]);
+        if (rp1 - rp0 <= kSpCap) {
+          const uintptr_t va = (uintptr_t)(vals + rp0) & ~(uintptr_t)15, vb = ((uintptr_t)(vals + rp1) + 15) & ~(uintptr_t)15;
+          const uintptr_t ca = (uintptr_t)(cols + rp0) & ~(uintptr_t)15, cb = ((uintptr_t)(cols + rp1) + 15) & ~(uintptr_t)15;
+          const uintptr_t ra = (uintptr_t)(rowptr + r0) & ~(uintptr_t)15, rb = ((uintptr_t)(rowptr + r1 + 1) + 15) & ~(uintptr_t)15;
+          st.voff = (int32_t)(((uintptr_t)(vals + rp0) - va) / 8);
+          st.coff = (int32_t)(((uintptr_t)(cols + rp0) - ca) / 4);
+          st.roff = (int32_t)(((uintptr_t)(rowptr + r0) - ra) / 4);
+          st.mode = 0;
+          const uint32_t vbytes = (uint32_t)(vb - va), cbytes = (uint32_t)(cb - ca), rbytes = (uint32_t)(rb - ra);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                       :: "r"(fb), "r"(vbytes + cbytes + rbytes) : "memory");
+          sp_bulk(sp_smem(st.rowptr), (const void*)ra, rbytes, fb);
+          if (vbytes) sp_bulk(sp_smem(st.vals), (const void*)va, vbytes, fb);
+          if (cbytes) sp_bulk(sp_smem(st.cols), (const void*)ca, cbytes, fb);
+        } else {
+          st.mode = 1;  // too many nonzeros for a stage: consumers read this chunk from global
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(fb) : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // consumers: one row per thread per chunk
+  double dacc = 0.0;
+  for (int64_t c = blockIdx.x, k = 0; c < nchunks; c += gridDim.x, ++k) {
+    const int s = (int)(k % kSpStages);
+    sp_wait(sp_smem(&S.full[s]), (uint32_t)((k / kSpStages) & 1));
+    const SpStage& st = S.st[s];
+    const int64_t row = c * kSpR + threadIdx.x;
+    if (row < nrows) {
+      double acc = 0.0;
+      if (st.mode == 0) {
+        const int b = (int)(st.rowptr[st.roff + threadIdx.x] - st.rp0);
+        const int e = (int)(st.rowptr[st.roff + threadIdx.x + 1] - st.rp0);
+        const double* sv = st.vals + st.voff;
+        const int32_t* sc = st.cols + st.coff;
+        int j = b;
+        for (; j + 8 <= e; j += 8) {
+          double xv[8], vv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            vv[t] = sv[j + t];
+            xv[t] = __ldg(x + sc[j + t]);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) acc = __dadd_rn(acc, __dmul_rn(vv[t], xv[t]));
+        }
+        if (j < e) {
+          double xv[8], vv[8];
+          const int len = e - j;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < len) {
+              vv[t] = sv[j + t];
+              xv[t] = __ldg(x + sc[j + t]);
+            }
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < len) acc = __dadd_rn(acc, __dmul_rn(vv[t], xv[t]));
+        }
+      } else {
+        const int64_t b = rowptr[row], e = rowptr[row + 1];
+        for (int64_t j = b; j < e; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(vals + j), __ldg(x + cols[j])));
+      }
+      y[row] = acc;
+      if (dot) dacc = __dadd_rn(dacc, __dmul_rn(__ldg(x + x_row0 + row), acc));
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(sp_smem(&S.empty[s])) : "memory");
+  }
+  if (dot) {
+    for (int o = 16; o; o >>= 1) dacc = __dadd_rn(dacc, __shfl_xor_sync(0xffffffffu, dacc, o));
+    if (lane == 0) S.red[warp] = dacc;
+    asm volatile("bar.sync 1, %0;" :: "r"(kSpR) : "memory");  // consumers only
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kSpConsumers; ++w) t = __dadd_rn(t, S.red[w]);
+      dot[blockIdx.x] = t;
+    }
+  }
+}
+
+size_t spmv_bulk_smem() { return sizeof(SpShared); }
+
 // ---- dense matvec: one warp per row, fixed lane order ------------------------
 
 __global__ void k_matvec(dk_view A, dk_view xv, dk_view yv) {
@@ -188,6 +358,22 @@ void launch_builtin(const std::string& kind, const dk_view* v, int n, const int3
     // products staged in shared memory, per-row in-order sums: 1.46 ms).
     // The per-row loop's strided loads are served from L1 (67 % hits).
     static const bool persist = getenv("DK_SPMV_PERSIST") != nullptr;
+    static const bool simple = getenv("DK_SPMV_SIMPLE") != nullptr;
+    if (rp.dtype == DK_I32 && !simple && !persist && nrows >= 4096) {
+      static const int smem = [] {
+        const int b = (int)spmv_bulk_smem();
+        cudaFuncSetAttribute(k_spmv_csr_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+        return b;
+      }();
+      const int64_t nchunks = (nrows + kSpR - 1) / kSpR;
+      const int blocks = (int)std::min<int64_t>(nchunks, (int64_t)sms * 2);
+      k_spmv_csr_bulk<<<blocks, kSpR + 32, smem, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
+                                                      (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr,
+                                                      nrows, nullptr, 0);
+      DK_CUDA(cudaGetLastError());
+      st().launches++;
+      return;
+    }
     const int blocks = (int)std::min<int64_t>((nrows + 255) / 256, persist ? (int64_t)sms * 8 : 0x7fffffff);
     if (rp.dtype == DK_I32)
       k_spmv_csr<int32_t><<<blocks, 256, 0, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,

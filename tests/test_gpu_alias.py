@@ -193,7 +193,8 @@ def _libm_pow():
 
 
 def test_pow_against_host_pow():
-    """'**' vs libm pow and np.power: exact on representable results, <= 1 ulp elsewhere.
+    """'**' vs libm pow and np.power: correctly rounded (exact on representable results), so within
+    1 ulp of either host implementation -- glibc's pow itself misrounds ~0.04 % of random inputs.
 
     np.power is host-dependent: on AVX-512 hosts numpy uses SVML, which differs
     from libm by 1 ulp on ~5 % of random inputs and on two special cases
@@ -212,7 +213,14 @@ def test_pow_against_host_pow():
     fin = np.isfinite(want) & (want != 0)
     ulp = np.abs(got[fin].view(np.int64) - want[fin].view(np.int64))
     assert ulp.max() <= 1
-    assert (ulp == 0).mean() > 0.9999
+    assert (ulp == 0).mean() > 0.999
+    # where the device and libm disagree, the device is the correctly rounded one (60-digit decimal)
+    from decimal import Decimal, getcontext
+
+    getcontext().prec = 60
+    idx = np.where(fin)[0][ulp != 0]
+    for i in idx[:2000]:
+        assert float(Decimal(float(x[i])) ** Decimal(float(y[i]))) == got[i], (x[i], y[i])
     assert np.abs(got[fin].view(np.int64) - npw[fin].view(np.int64)).max() <= 1
     assert same_bits(got[~fin], want[~fin])
     ints = slice(2 * n, 4 * n)  # integer bases and exponents: exact whenever representable
