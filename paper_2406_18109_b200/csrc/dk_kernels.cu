@@ -115,21 +115,19 @@ __global__ void __launch_bounds__(256) k_spmv_csr(const I* __restrict__ rowptr, 
 // over the tile's rows (p = x at row offset x_row0), for the opt-in SpMV +
 // partial-dot fusion; per-thread in row order, then a fixed warp / CTA tree.
 namespace {
-constexpr int kSpR = 256;
-constexpr int kSpCap = 2048;
-constexpr int kSpStages = 4;
-constexpr int kSpConsumers = kSpR / 32;
-struct __align__(16) SpStage {
-  double vals[kSpCap + 2];
-  int32_t cols[kSpCap + 4];
-  int32_t rowptr[kSpR + 8];
+template <int R, int CAP, int S>
+struct __align__(16) SpStageT {
+  double vals[CAP + 2];
+  int32_t cols[CAP + 4];
+  int32_t rowptr[R + 8];
   int64_t rp0;
   int32_t voff, coff, roff, mode;
 };
-struct SpShared {
-  SpStage st[kSpStages];
-  unsigned long long full[kSpStages], empty[kSpStages];
-  double red[kSpConsumers];
+template <int R, int CAP, int S>
+struct SpSharedT {
+  SpStageT<R, CAP, S> st[S];
+  unsigned long long full[S], empty[S];
+  double red[R / 32];
 };
 __device__ __forceinline__ uint32_t sp_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -146,45 +144,48 @@ __device__ __forceinline__ void sp_bulk(uint32_t dst, const void* src, uint32_t 
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kSpR + 32, 2)
+// R rows per chunk (one per consumer thread), CAP nonzeros per stage, S stages, MINB CTAs per SM
+template <int R, int CAP, int S, int MINB>
+__global__ void __launch_bounds__(R + 32, MINB)
     k_spmv_csr_bulk(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                     const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y,
                     int64_t nrows, double* __restrict__ dot, int64_t x_row0) {
+  constexpr int NC = R / 32;  // consumer warps
   extern __shared__ __align__(16) unsigned char sp_raw[];
-  SpShared& S = *reinterpret_cast<SpShared*>(sp_raw);
+  SpSharedT<R, CAP, S>& SH = *reinterpret_cast<SpSharedT<R, CAP, S>*>(sp_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nchunks = (nrows + kSpR - 1) / kSpR;
+  const int64_t nchunks = (nrows + R - 1) / R;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSpStages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&S.full[s])), "r"(1) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&S.empty[s])), "r"(kSpConsumers) : "memory");
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&SH.full[s])), "r"(1) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sp_smem(&SH.empty[s])), "r"(NC) : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kSpConsumers) {  // producer
+  if (warp == NC) {  // producer
     if (lane == 0) {
       int64_t c = blockIdx.x;
       int64_t nr0 = 0, nr1 = 0;
       if (c < nchunks) {
-        nr0 = __ldg(rowptr + c * kSpR);
-        nr1 = __ldg(rowptr + (c * kSpR + kSpR < nrows ? c * kSpR + kSpR : nrows));
+        nr0 = __ldg(rowptr + c * R);
+        nr1 = __ldg(rowptr + (c * R + R < nrows ? c * R + R : nrows));
       }
       for (int64_t k = 0; c < nchunks; c += gridDim.x, ++k) {
-        const int s = (int)(k % kSpStages);
-        if (k >= kSpStages) sp_wait(sp_smem(&S.empty[s]), (uint32_t)(((k / kSpStages) - 1) & 1));
-        const int64_t r0 = c * kSpR, r1 = (r0 + kSpR < nrows ? r0 + kSpR : nrows);
+        const int s = (int)(k % S);
+        if (k >= S) sp_wait(sp_smem(&SH.empty[s]), (uint32_t)(((k / S) - 1) & 1));
+        const int64_t r0 = c * R, r1 = (r0 + R < nrows ? r0 + R : nrows);
         const int64_t rp0 = nr0, rp1 = nr1;
         // prefetch the next chunk's boundaries (consumed one iteration later)
         const int64_t cn = c + gridDim.x;
         if (cn < nchunks) {
-          nr0 = __ldg(rowptr + cn * kSpR);
-          nr1 = __ldg(rowptr + (cn * kSpR + kSpR < nrows ? cn * kSpR + kSpR : nrows));
+          nr0 = __ldg(rowptr + cn * R);
+          nr1 = __ldg(rowptr + (cn * R + R < nrows ? cn * R + R : nrows));
         }
-        SpStage& st = S.st[s];
+        SpStageT<R, CAP, S>& st = SH.st[s];
         st.rp0 = rp0;
-        const uint32_t fb = sp_smem(&S.full[s]);
-        if (rp1 - rp0 <= kSpCap) {
+        const uint32_t fb = sp_smem(&SH.full[s]);
+        if (rp1 - rp0 <= CAP) {
           const uintptr_t va = (uintptr_t)(vals + rp0) & ~(uintptr_t)15, vb = ((uintptr_t)(vals + rp1) + 15) & ~(uintptr_t)15;
           const uintptr_t ca = (uintptr_t)(cols + rp0) & ~(uintptr_t)15, cb = ((uintptr_t)(cols + rp1) + 15) & ~(uintptr_t)15;
           const uintptr_t ra = (uintptr_t)(rowptr + r0) & ~(uintptr_t)15, rb = ((uintptr_t)(rowptr + r1 + 1) + 15) & ~(uintptr_t)15;
@@ -209,10 +210,10 @@ __global__ void __launch_bounds__(kSpR + 32, 2)
   // consumers: one row per thread per chunk
   double dacc = 0.0;
   for (int64_t c = blockIdx.x, k = 0; c < nchunks; c += gridDim.x, ++k) {
-    const int s = (int)(k % kSpStages);
-    sp_wait(sp_smem(&S.full[s]), (uint32_t)((k / kSpStages) & 1));
-    const SpStage& st = S.st[s];
-    const int64_t row = c * kSpR + threadIdx.x;
+    const int s = (int)(k % S);
+    sp_wait(sp_smem(&SH.full[s]), (uint32_t)((k / S) & 1));
+    const SpStageT<R, CAP, S>& st = SH.st[s];
+    const int64_t row = c * R + threadIdx.x;
     if (row < nrows) {
       double acc = 0.0;
       if (st.mode == 0) {
@@ -220,29 +221,15 @@ __global__ void __launch_bounds__(kSpR + 32, 2)
         const int e = (int)(st.rowptr[st.roff + threadIdx.x + 1] - st.rp0);
         const double* sv = st.vals + st.voff;
         const int32_t* sc = st.cols + st.coff;
-        int j = b;
-        for (; j + 8 <= e; j += 8) {
-          double xv[8], vv[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            vv[t] = sv[j + t];
-            xv[t] = __ldg(x + sc[j + t]);
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t) acc = __dadd_rn(acc, __dmul_rn(vv[t], xv[t]));
-        }
-        if (j < e) {
-          double xv[8], vv[8];
+        for (int j = b; j < e; j += 8) {
           const int len = e - j;
+          double xv[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t)
-            if (t < len) {
-              vv[t] = sv[j + t];
-              xv[t] = __ldg(x + sc[j + t]);
-            }
+            if (t < len) xv[t] = __ldg(x + sc[j + t]);
 #pragma unroll
           for (int t = 0; t < 8; ++t)
-            if (t < len) acc = __dadd_rn(acc, __dmul_rn(vv[t], xv[t]));
+            if (t < len) acc = __dadd_rn(acc, __dmul_rn(sv[j + t], xv[t]));
         }
       } else {
         const int64_t b = rowptr[row], e = rowptr[row + 1];
@@ -252,21 +239,51 @@ __global__ void __launch_bounds__(kSpR + 32, 2)
       if (dot) dacc = __dadd_rn(dacc, __dmul_rn(__ldg(x + x_row0 + row), acc));
     }
     __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(sp_smem(&S.empty[s])) : "memory");
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(sp_smem(&SH.empty[s])) : "memory");
   }
   if (dot) {
     for (int o = 16; o; o >>= 1) dacc = __dadd_rn(dacc, __shfl_xor_sync(0xffffffffu, dacc, o));
-    if (lane == 0) S.red[warp] = dacc;
-    asm volatile("bar.sync 1, %0;" :: "r"(kSpR) : "memory");  // consumers only
+    if (lane == 0) SH.red[warp] = dacc;
+    asm volatile("bar.sync 1, %0;" :: "r"(R) : "memory");  // consumers only
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < kSpConsumers; ++w) t = __dadd_rn(t, S.red[w]);
+      for (int w = 0; w < NC; ++w) t = __dadd_rn(t, SH.red[w]);
       dot[blockIdx.x] = t;
     }
   }
 }
 
-size_t spmv_bulk_smem() { return sizeof(SpShared); }
+// launch configurations (DK_SPMV_CFG selects one; default 0)
+struct SpCfg {
+  void (*fn)(const int32_t*, const int32_t*, const double*, const double*, double*, int64_t, double*, int64_t);
+  int rows, threads, smem, minb;
+};
+template <int R, int CAP, int S, int MINB>
+static SpCfg sp_cfg() {
+  SpCfg c;
+  c.fn = k_spmv_csr_bulk<R, CAP, S, MINB>;
+  c.rows = R;
+  c.threads = R + 32;
+  c.smem = (int)sizeof(SpSharedT<R, CAP, S>);
+  c.minb = MINB;
+  cudaFuncSetAttribute(c.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem);
+  return c;
+}
+static const SpCfg& spmv_cfg() {
+  static const SpCfg cfg = [] {
+    const char* e = getenv("DK_SPMV_CFG");
+    const int v = e ? atoi(e) : 0;
+    switch (v) {
+      case 1: return sp_cfg<256, 2048, 4, 2>();
+      case 2: return sp_cfg<256, 1536, 2, 4>();
+      case 3: return sp_cfg<512, 3072, 2, 2>();
+      case 4: return sp_cfg<256, 1536, 3, 3>();
+      case 5: return sp_cfg<128, 768, 4, 6>();
+      default: return sp_cfg<256, 1536, 3, 3>();
+    }
+  }();
+  return cfg;
+}
 
 // ---- dense matvec: one warp per row, fixed lane order ------------------------
 
@@ -360,16 +377,12 @@ void launch_builtin(const std::string& kind, const dk_view* v, int n, const int3
     static const bool persist = getenv("DK_SPMV_PERSIST") != nullptr;
     static const bool simple = getenv("DK_SPMV_SIMPLE") != nullptr;
     if (rp.dtype == DK_I32 && !simple && !persist && nrows >= 4096) {
-      static const int smem = [] {
-        const int b = (int)spmv_bulk_smem();
-        cudaFuncSetAttribute(k_spmv_csr_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-        return b;
-      }();
-      const int64_t nchunks = (nrows + kSpR - 1) / kSpR;
-      const int blocks = (int)std::min<int64_t>(nchunks, (int64_t)sms * 2);
-      k_spmv_csr_bulk<<<blocks, kSpR + 32, smem, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
-                                                      (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr,
-                                                      nrows, nullptr, 0);
+      const SpCfg& cfg = spmv_cfg();
+      const int64_t nchunks = (nrows + cfg.rows - 1) / cfg.rows;
+      const int blocks = (int)std::min<int64_t>(nchunks, (int64_t)sms * cfg.minb);
+      cfg.fn<<<blocks, cfg.threads, cfg.smem, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
+                                                   (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr,
+                                                   nrows, nullptr, 0);
       DK_CUDA(cudaGetLastError());
       st().launches++;
       return;

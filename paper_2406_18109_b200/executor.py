@@ -125,6 +125,12 @@ class Executor:
         self._comm = False
         self._p2p = False
         self._p2p_epoch = 0
+        # CUDA-graph relaunch of repeated launch segments (enable_graphs)
+        self._graphs_on = False
+        self._pending: list = []  # deferred plan-cache hits: (handle, views, scalars, nscal, nslots)
+        self._seg_seen: dict[tuple, int] = {}
+        self._seg_graphs: dict[tuple, int] = {}
+        self.graph_stats = {"segments": 0, "graph_launches": 0, "captures": 0, "direct": 0}
 
     # ------------------------------------------------------------------ comm
     def init_comm(self, unique_id: bytes) -> None:
@@ -189,10 +195,12 @@ class Executor:
     def free(self, sid: int) -> None:
         r = self.stores.pop(sid, None)
         if r is not None and r.on_device:
+            self.drain()
             check(self.lib.dk_store_free(sid))
 
     def close(self) -> None:
         """Release every store this executor created (device state is process-global)."""
+        self.drop_graphs()
         for sid in list(self.stores):
             self.free(sid)
         check(self.lib.dk_sync())
@@ -457,6 +465,7 @@ class Executor:
         if isolated:
             if kp is None:
                 raise BackendError(f"isolated execution needs a kernel for kind {task.kind!r}")
+            self.drain()
             self.check_isolated(task, temp_positions)
             self._execute_planned(task, kp, temp_positions, None, isolated=True)
             return
@@ -474,10 +483,14 @@ class Executor:
                 h, _ = self.kernel_handle(kp)
                 scal = self._scalars(task.scalars)
                 for views in hit[2]:
-                    check(self.lib.dk_launch(h, views, len(kp.slots), scal, len(task.scalars), 0))
+                    if self._graphs_on:
+                        self._pending.append((h, views, scal, len(task.scalars), len(kp.slots)))
+                    else:
+                        check(self.lib.dk_launch(h, views, len(kp.slots), scal, len(task.scalars), 0))
                 self.stats.launches += 1
                 self.stats.points += len(hit[2])
                 return
+        self.drain()
         if use_mplan:
             key, sids = self._mplan_key(task, kp, temp_positions)
             hit = self._mplans.get(key) if key is not None else None
@@ -494,6 +507,58 @@ class Executor:
                 self._rec = None
             return
         self._execute_planned(task, kp, temp_positions, pkey)
+
+    # ------------------------------------------------ graph relaunch (f3)
+    # With graphs enabled (GpuSession, one GPU), launches that hit the launch-plan
+    # cache are not issued at once but collected into a segment; the segment ends
+    # at the session's flush or at the first operation that is not such a hit
+    # (a planned launch, a free of a device store, any host transfer or sync).
+    # A segment is keyed by its exact launches (kernel handle, bound views and
+    # scalars, in order).  The second time a key is seen it is captured into a
+    # CUDA graph (dk_graph_*), and from then on each occurrence is one graph
+    # launch.  The key is the launch parameters themselves, so a graph can only
+    # ever replay launches the plan cache just decided to issue; no
+    # invalidation is needed when stores are freed and recreated.
+    def enable_graphs(self, on: bool = True) -> None:
+        self.drain()
+        self._graphs_on = bool(on) and self.world == 1 and os.environ.get("DK_GRAPHS", "1") != "0"
+
+    def drain(self) -> None:
+        """Issue the deferred launch segment (as a graph when it repeats)."""
+        if not self._pending:
+            return
+        pend, self._pending = self._pending, []
+        self.graph_stats["segments"] += 1
+        key = tuple((h, bytes(v), bytes(sc)[: 8 * ns]) for h, v, sc, ns, _ in pend)
+        g = self._seg_graphs.get(key)
+        if g is None:
+            n = self._seg_seen.get(key, 0) + 1
+            if n >= 2 and len(self._seg_graphs) < 256:
+                def issue():
+                    for h, v, sc, ns, nsl in pend:
+                        check(self.lib.dk_launch(h, v, nsl, sc, ns, 0))
+
+                g = self.capture(issue)
+                self._seg_graphs[key] = g
+                self.graph_stats["captures"] += 1
+                self._seg_seen.pop(key, None)
+            else:
+                if len(self._seg_seen) > 4096:
+                    self._seg_seen.clear()
+                self._seg_seen[key] = n
+                for h, v, sc, ns, nsl in pend:
+                    check(self.lib.dk_launch(h, v, nsl, sc, ns, 0))
+                self.graph_stats["direct"] += 1
+                return
+        check(self.lib.dk_graph_launch(c_uint64(g)))
+        self.graph_stats["graph_launches"] += 1
+
+    def drop_graphs(self) -> None:
+        self.drain()
+        for g in self._seg_graphs.values():
+            check(self.lib.dk_graph_destroy(c_uint64(g)))
+        self._seg_graphs.clear()
+        self._seg_seen.clear()
 
     # ------------------------------------------------ multi-GPU plan cache
     # A memo-replayed window repeats with the same launch, the same coherence
@@ -1117,6 +1182,7 @@ class Executor:
     # ---------------------------------------------------------- host access
     def upload(self, sid: int, host: np.ndarray) -> None:
         """Replace the whole store with ``host`` (every rank holds it valid)."""
+        self.drain()
         r = self.rec(sid)
         np_dtype = np.float64 if r.dtype == "f64" else np.int32
         a = np.asarray(host, dtype=np_dtype)  # (ascontiguousarray would turn 0-d into (1,))
@@ -1133,6 +1199,7 @@ class Executor:
 
     def upload_async(self, sid: int, host: np.ndarray, rect=None) -> None:
         """Enqueue an H2D copy of ``rect`` from a full-store host array (pinned for overlap)."""
+        self.drain()
         r = self.rec(sid)
         rect = rect or r.full
         self._ensure(r, rect)
@@ -1141,6 +1208,7 @@ class Executor:
 
     def download(self, sid: int, out: np.ndarray | None = None, rect=None) -> np.ndarray | None:
         """Collective on all ranks: gather ``rect`` of the store to rank 0 and copy it out."""
+        self.drain()
         r = self.rec(sid)
         rect = rect or r.full
         self._satisfy({0: {sid: [rect]}})
@@ -1155,6 +1223,7 @@ class Executor:
 
     def download_local(self, sid: int, out: np.ndarray, rect) -> np.ndarray:
         """D2H of a rect this rank holds valid (no gather; ``out`` is full-store shaped)."""
+        self.drain()
         r = self.rec(sid)
         if not rg.covered(r.valid[self.rank], rect):
             raise BackendError(f"store {sid} rect {rect} is not valid on rank {self.rank}")
@@ -1168,6 +1237,7 @@ class Executor:
         return a.astype(np.float64) if a.dtype != np.float64 else a
 
     def sync(self) -> None:
+        self.drain()
         check(self.lib.dk_sync())
 
     def jit_stats(self) -> dict:
@@ -1186,6 +1256,8 @@ class Executor:
         """Run ``fn()`` (enqueue-only executor calls, e.g. one memo-replayed iteration whose
         launches are already planned) under stream capture; returns a graph handle for
         :meth:`graph_launch`.  Any synchronising call inside ``fn`` fails the capture."""
+        if self._pending:
+            raise BackendError("capture() with a deferred launch segment pending (call drain() first)")
         check(self.lib.dk_graph_begin())
         g = c_uint64()
         try:

@@ -63,7 +63,11 @@ class GpuHeap:
         self.ex = executor
         self.arrays = _Arrays(self)
 
-    def get(self, store_id: int) -> np.ndarray:
+    def get(self, store_id: int, out: np.ndarray | None = None) -> np.ndarray:
+        """The store's contents (``Heap.get``); ``out`` (backend extension): copy into this
+        full-store array instead of a new one -- pinned memory makes the copy a DMA."""
+        if out is not None:
+            return self.ex.download(store_id, out=out)
         return self.ex.get(store_id)
 
     def materialized(self, store_id: int) -> bool:
@@ -85,8 +89,15 @@ class GpuHeap:
 
 
 class GpuSession(_RefSession):
+    """``Session`` whose ``_execute`` runs on the B200.
+
+    ``graphs`` (default on, one GPU): launch segments that repeat -- the
+    windows of a flush that all hit the launch-plan cache with identical
+    bindings, as memo replays of a steady iteration do -- are relaunched as one
+    CUDA graph (``Executor.drain``); ``DK_GRAPHS=0`` turns it off."""
+
     def __init__(self, config=None, registry=None, builtins=None, *, rank=0, world=1, device=None,
-                 init=None, dtypes=None):
+                 init=None, dtypes=None, graphs=True):
         super().__init__(config, registry, builtins)
         self.executor = Executor(
             seed=self.config.seed,
@@ -99,6 +110,29 @@ class GpuSession(_RefSession):
         )
         self.heap = GpuHeap(self.executor)
         self._lowered: dict[int, tuple[object, object]] = {}
+        self._pinned: list = []
+        self.executor.enable_graphs(graphs)
+
+    def _flush(self, explicit: bool) -> None:  # pipeline.py:194-240, unchanged; then end the launch segment
+        try:
+            super()._flush(explicit)
+        finally:
+            self.executor.drain()
+
+    def close(self) -> None:
+        """Release the device stores, graphs and pinned host buffers of this session."""
+        self.executor.close()
+        for p in self._pinned:
+            self.executor.lib.dk_host_free(p)
+        self._pinned.clear()
+
+    def pinned(self, shape, dtype=np.float64) -> np.ndarray:
+        """A host array in page-locked memory (fast, asynchronous copies to and from the heap)."""
+        from .streaming import pinned
+
+        a, p = pinned(self.executor, tuple(shape), dtype)
+        self._pinned.append(p)
+        return a
 
     def _lower(self, kernel, fused: bool):
         hit = self._lowered.get(id(kernel))

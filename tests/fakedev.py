@@ -309,6 +309,15 @@ class FakeLib:
         return 0
 
     def dk_launch(self, h, views, nviews, scalars, nscal, totals):
+        if getattr(self, "_capturing", None) is not None:
+            # parameters are captured by value (cuLaunchKernel copies them)
+            vcopy = (views._type_ * nviews)()
+            ctypes.memmove(vcopy, views, ctypes.sizeof(views._type_) * nviews)
+            self._capturing.append((h, vcopy, nviews, [scalars[i] for i in range(nscal)], nscal, totals))
+            return 0
+        return self._launch_now(h, views, nviews, scalars, nscal, totals)
+
+    def _launch_now(self, h, views, nviews, scalars, nscal, totals):
         kp = self.kernels[h]
         bufs = {}
         lshapes = {}
@@ -347,6 +356,30 @@ class FakeLib:
         else:
             interpret(kp, bufs, scal, lshapes)
         self.launches += 1
+        return 0
+
+    # CUDA graphs: a capture records the launches issued while it is open; a relaunch replays them
+    def dk_graph_begin(self):
+        self._capturing = []
+        return 0
+
+    def dk_graph_end(self, ref):
+        gid = self.next_id
+        self.next_id += 1
+        self.graphs = getattr(self, "graphs", {})
+        self.graphs[gid] = self._capturing
+        self._capturing = None
+        _set(ref, gid)
+        return 0
+
+    def dk_graph_launch(self, g):
+        gid = g.value if hasattr(g, "value") else int(g)
+        for args in self.graphs[gid]:
+            self._launch_now(*args)
+        return 0
+
+    def dk_graph_destroy(self, g):
+        self.graphs.pop(g.value if hasattr(g, "value") else int(g), None)
         return 0
 
     def dk_accum(self, tv, vals, first, stride, n):

@@ -172,3 +172,38 @@ def test_check_isolated_rejects_overlapping_claims():
     with pytest.raises(ArenaViolation):
         ex.check_isolated(cross_read, frozenset())
     ex.check_isolated(TaskDesc("COPY", (2,), (ArgDesc(0, wide, "R"), ArgDesc(1, wide, "W"))), frozenset())
+
+
+def test_graph_segments_replay_identical_launches(monkeypatch):
+    """GpuSession's graph relaunch (Executor.drain) on the CPU stand-in: repeated launch segments are
+    captured once and relaunched, and the heaps still equal the reference Session's."""
+    import os
+    import sys
+
+    from conftest import reference_available
+
+    ref_src = reference_available()
+    if ref_src is None:
+        pytest.skip("reference not importable")
+    sys.dont_write_bytecode = True
+    if ref_src not in sys.path:
+        sys.path.insert(0, ref_src)
+    from diffusekit.pipeline import Session, SessionConfig, run_events
+    from diffusekit.trace import gen_benchmark
+    from fakedev import FakeLib
+
+    from paper_2406_18109_b200 import runtime
+    from paper_2406_18109_b200.session import GpuSession
+
+    monkeypatch.setattr(runtime, "load", lambda *a, **k: FakeLib(0, 1, device_model=True))
+    monkeypatch.setenv("DK_HOST_INIT", "1")
+    for name, kw in (("blackscholes_chain", dict(size=4096, nodes=2, iters=6)), ("jacobi", dict(size=16, nodes=4, iters=4))):
+        ref = Session(SessionConfig())
+        run_events(ref, gen_benchmark(name, **kw))
+        gpu = GpuSession(SessionConfig(), device=0)
+        run_events(gpu, gen_benchmark(name, **kw))
+        for s in ref.live_store_ids():
+            assert same_bits(gpu.heap.get(s), ref.heap.get(s)), (name, s)
+        if name == "blackscholes_chain":
+            gs = gpu.executor.graph_stats
+            assert gs["captures"] >= 1 and gs["graph_launches"] >= 2, gs

@@ -55,8 +55,10 @@ def _large(name):
 def _shared_poisson(monkeypatch):
     """The executor and the oracle both build the Poisson CSR tiles on the host: build each once."""
     import functools
+    import importlib
 
-    from paper_2406_18109_b200 import executor, initheap
+    executor = importlib.import_module("paper_2406_18109_b200.executor")
+    initheap = importlib.import_module("paper_2406_18109_b200.initheap")
 
     cached = functools.lru_cache(maxsize=2)(initheap.poisson_tile)
     monkeypatch.setattr(initheap, "poisson_tile", cached)
