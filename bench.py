@@ -580,11 +580,11 @@ def barrier(torch, world):
         dist.barrier()
 
 
-def make_executor(trace, rank, world, local, torch):
+def make_executor(trace, rank, world, local, torch, fuse_spmv_dot=None):
     from paper_2406_18109_b200.executor import Executor
 
     ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, rank=rank, world=world,
-                  device=local)
+                  device=local, fuse_spmv_dot=fuse_spmv_dot)
     if world > 1:
         import torch.distributed as dist
 
@@ -810,9 +810,9 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if peaks else "fallback"
 
-    def one(wl, mode, with_clock=False, with_e2e=False, plan=None, steps=None):
+    def one(wl, mode, with_clock=False, with_e2e=False, plan=None, steps=None, fuse_spmv_dot=None):
         trace = load_trace(plan or f"{wl}_{mode}_n{world}")
-        ex = make_executor(trace, rank, world, local, torch)
+        ex = make_executor(trace, rank, world, local, torch, fuse_spmv_dot=fuse_spmv_dot)
         ext = torch.cuda.ExternalStream(ex.stream())
         sampler = ClockSampler(local) if with_clock else None
         try:
@@ -946,6 +946,20 @@ def run_ours(args):
                     "result_check": f["check"],
                     "unfused_result_check": u["check"],
                 }
+                if w2 in ("cg", "pcg") and world == 1:
+                    # opt-in SpMV + partial-dot epilogue (BASELINE configs[3] "fused SpMV+dot+axpy"):
+                    # same plan, the [DOT, DOT] window's p.q comes from the SpMV kernel
+                    try:
+                        e = one(w2, "fused", fuse_spmv_dot=True)
+                        others[w2]["fused_spmv_dot"] = {
+                            "iter_s": round(world * K / (e["ms"] / 1e3), 3),
+                            "ms_per_step": round(e["ms"] / K, 4),
+                            "per_exec_ms": e["dom"]["per_exec_ms"] if e["dom"] else None,
+                            "result_check": e["check"],
+                            "note": "DK_FUSE_SPMV_DOT=1: SPMV_CSR also emits per-CTA partials of p.q; the "
+                                    "[DOT,DOT] window drops that reduction (2 x 0.537 GB less traffic per iteration)"}
+                    except Exception as exc:  # noqa: BLE001
+                        others[w2]["fused_spmv_dot"] = {"error": f"{type(exc).__name__}: {exc}"}
                 if rank == 0 and world == 1 and not args.quick:
                     try:
                         others[w2]["cpu_baseline"] = run_cpu_baseline(w2, "fused", budget_s=8.0)

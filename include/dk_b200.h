@@ -143,6 +143,14 @@ int dk_accum(const dk_view* target, uint64_t vals, int64_t first, int64_t stride
 /* opaque kinds: kind = "MATVEC" | "SPMV" | "NORM" | "OPAQUE" | "SPMV_CSR" */
 int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t* writes);
 
+/* SPMV_CSR with the opt-in partial-dot epilogue (DK_FUSE_SPMV_DOT=1; backend-only, it
+ * changes which launch computes the following window's p.q, never the fusion plan):
+ * views as dk_builtin("SPMV_CSR"); also writes per-CTA partials of sum_i x[x_row0+i]*y[i]
+ * (i over this tile's rows, each partial a fixed in-order sum) to `parts` (device, room for
+ * 4096 doubles) and their count to *nparts.  Replaces, for that window, the
+ * DOT(p, q -> pq) reduction of the cg_like stream (trace.py:384-386). */
+int dk_spmv_csr_dot(const dk_view* views, uint64_t parts, int64_t x_row0, int* nparts);
+
 /* multi-GPU (NCCL over NVLink/NVSwitch); one rank per process */
 int dk_comm_unique_id(uint8_t* out128);
 int dk_comm_init(int rank, int world, const uint8_t* id128);

@@ -346,6 +346,30 @@ static void check_f64(const dk_view& v, const char* what) {
   if (v.dtype != DK_F64) fail(DK_ERR_UNSUPPORTED, "%s: expected an f64 view", what);
 }
 
+int launch_spmv_csr_dot(const dk_view* v, double* parts, int64_t x_row0, cudaStream_t s) {
+  const dk_view &rp = v[0], &cl = v[1], &vl = v[2], &x = v[3], &y = v[4];
+  check_f64(vl, "SPMV_CSR vals");
+  check_f64(x, "SPMV_CSR x");
+  check_f64(y, "SPMV_CSR y");
+  if (rp.dtype != DK_I32 || cl.dtype != DK_I32) fail(DK_ERR_UNSUPPORTED, "SPMV_CSR+dot needs int32 indices");
+  if (x.rank != 1 || y.rank != 1 || x.stride[0] != 1 || y.stride[0] != 1)
+    fail(DK_ERR_UNSUPPORTED, "SPMV_CSR+dot needs contiguous rank-1 x and y");
+  const int64_t nrows = view_volume(y);
+  if (view_volume(rp) != nrows + 1) fail(DK_ERR_ARG, "SPMV_CSR: rowptr has %lld entries for %lld rows",
+                                         (long long)view_volume(rp), (long long)nrows);
+  if (x_row0 < 0 || x_row0 + nrows > x.ext[0]) fail(DK_ERR_ARG, "SPMV_CSR+dot: x rows out of range");
+  if (nrows == 0) return 0;
+  const SpCfg& cfg = spmv_cfg();
+  const int64_t nchunks = (nrows + cfg.rows - 1) / cfg.rows;
+  const int blocks = (int)std::min<int64_t>(std::min<int64_t>(nchunks, (int64_t)st().sm_count * cfg.minb), 4096);
+  cfg.fn<<<blocks, cfg.threads, cfg.smem, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
+                                               (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr, nrows,
+                                               parts, x_row0);
+  DK_CUDA(cudaGetLastError());
+  st().launches++;
+  return blocks;
+}
+
 void launch_builtin(const std::string& kind, const dk_view* v, int n, const int32_t* writes, cudaStream_t s) {
   const int sms = st().sm_count;
   if (kind == "SPMV_CSR") {

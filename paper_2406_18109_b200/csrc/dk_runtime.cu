@@ -524,6 +524,13 @@ int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t
   });
 }
 
+int dk_spmv_csr_dot(const dk_view* views, uint64_t parts, int64_t x_row0, int* nparts) {
+  return guard([&] {
+    require_init();
+    *nparts = launch_spmv_csr_dot(views, (double*)parts, x_row0, st().stream);
+  });
+}
+
 }  // extern "C"
 
 // ---- CUDA graphs of memo-hit windows --------------------------

@@ -98,6 +98,7 @@ class Executor:
         device: int | None = None,
         shape_of=None,
         lib=None,
+        fuse_spmv_dot: bool | None = None,
     ) -> None:
         # ``lib``: an object with the C-ABI's functions; only the test-suite's CPU
         # stand-in passes one.  The product always loads libdk_b200.so.
@@ -131,6 +132,12 @@ class Executor:
         self._seg_seen: dict[tuple, int] = {}
         self._seg_graphs: dict[tuple, int] = {}
         self.graph_stats = {"segments": 0, "graph_launches": 0, "captures": 0, "direct": 0}
+        # opt-in SpMV + partial-dot epilogue (backend-only; the fusion plan is unchanged)
+        if fuse_spmv_dot is None:
+            fuse_spmv_dot = os.environ.get("DK_FUSE_SPMV_DOT", "0") == "1"
+        self.fuse_spmv_dot = bool(fuse_spmv_dot) and world == 1
+        self._sd = None  # partials of the last SPMV_CSR, waiting for the window that reduces p.q
+        self.spmv_dot_stats = {"spmv": 0, "consumed": 0}
 
     # ------------------------------------------------------------------ comm
     def init_comm(self, unique_id: bytes) -> None:
@@ -192,7 +199,15 @@ class Executor:
         lo, hi = rg.bbox_flat(r.shape, rect)
         check(self.lib.dk_store_ensure(r.sid, lo, hi))
 
+    def _drop_sd(self) -> None:
+        if self._sd is not None:
+            for _rect, ptr, _n in self._sd["pts"].values():
+                check(self.lib.dk_scratch_free(ptr))
+            self._sd = None
+
     def free(self, sid: int) -> None:
+        if self._sd is not None and sid in (self._sd["x"], self._sd["y"]):
+            self._drop_sd()
         r = self.stores.pop(sid, None)
         if r is not None and r.on_device:
             self.drain()
@@ -201,6 +216,7 @@ class Executor:
     def close(self) -> None:
         """Release every store this executor created (device state is process-global)."""
         self.drop_graphs()
+        self._drop_sd()
         for sid in list(self.stores):
             self.free(sid)
         check(self.lib.dk_sync())
@@ -462,6 +478,16 @@ class Executor:
         if kp is None and task.kind not in BUILTIN_KINDS:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
+        if self._sd is not None:
+            sd, self._sd = self._sd, None
+            try:
+                if kp is not None and not isolated:
+                    self.drain()
+                    self._execute_planned(task, kp, temp_positions, None, spmv_dot=sd)
+                    return
+            finally:
+                for _rect, ptr, _n in sd["pts"].values():
+                    check(self.lib.dk_scratch_free(ptr))
         if isolated:
             if kp is None:
                 raise BackendError(f"isolated execution needs a kernel for kind {task.kind!r}")
@@ -725,7 +751,7 @@ class Executor:
                         f"point {p} of {task.kind} reads store {a.store} cells written by another point")
 
     def _execute_planned(self, task: TaskDesc, kp: KProg | None, temp_positions, pkey,
-                         isolated: bool = False) -> None:
+                         isolated: bool = False, spmv_dot=None) -> None:
         pts = list(task.points())
         V = len(pts)
         prank = [self.point_rank(i, V) for i in range(V)]
@@ -785,7 +811,7 @@ class Executor:
         if kp is None:
             self._run_builtin(task, pts, mine, rects, prank)
         else:
-            recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces, isolated)
+            recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces, isolated, spmv_dot)
             if recorded is not None and self.world == 1 and pkey is not None:
                 # launch-plan cache: a memo-replayed window over the same
                 # stores re-launches with the bound views as they are
@@ -919,11 +945,53 @@ class Executor:
             check(self.lib.dk_launch(h, pair, 2, self._scalars(()), 0, 0))
         return dst, p.value
 
-    def _run_kernel(self, task, kp, mine, prank, rects, temp_positions, reduces, isolated=False) -> None:
+    def _spmv_dot_match(self, task, kp, mine, rects, sd):
+        """The reduce statement ``t += sum(p * q)`` this window would compute from the SpMV's own
+        x-tile and result (same rects), if any: (nest, stmt index, target slot)."""
+        for n, (_dom, _rank, stmts) in enumerate(kp.nests):
+            for k, st in enumerate(stmts):
+                if st[0] != "reduce":
+                    continue
+                e = st[2]
+                if e[0] != "bin" or e[1] != "*" or e[2][0] != "ld" or e[3][0] != "ld":
+                    continue
+                a, b = e[2][1], e[3][1]
+                if kp.slots[a].local or kp.slots[b].local or any(e[2][2]) or any(e[3][2]):
+                    continue
+                sa, sb = task.args[kp.slots[a].arg].store, task.args[kp.slots[b].arg].store
+                if {sa, sb} != {sd["x"], sd["y"]} or sa == sb:
+                    continue
+                if sum(1 for _, _, sts in kp.nests for t in sts if t[0] == "reduce" and t[1] == st[1]) != 1:
+                    continue
+                if len(stmts) < 2 or self.shape(task.args[kp.slots[st[1]].arg].store) != ():
+                    continue
+                if set(mine) != set(sd["pts"]):
+                    continue
+                if all(rects[i][kp.slots[a].arg] == sd["pts"][i][0] == rects[i][kp.slots[b].arg] for i in mine):
+                    return n, k, st[1]
+        return None
+
+    def _run_kernel(self, task, kp, mine, prank, rects, temp_positions, reduces, isolated=False,
+                    spmv_dot=None) -> None:
         if len(kp.scalar_names) != len(task.scalars):
             raise BackendError(
                 f"task {task.kind} carries {len(task.scalars)} scalars, kernel expects {len(kp.scalar_names)}"
             )
+        sd_fold = None
+        if spmv_dot is not None and self.world == 1:
+            m = self._spmv_dot_match(task, kp, mine, rects, spmv_dot)
+            if m is not None:
+                n, k, tslot = m
+                key = (id(kp), "spmv_dot", n, k)
+                hit = self._alias_k.get(key)
+                if hit is None or hit[0] is not kp:
+                    nests = list(kp.nests)
+                    dom, rank, stmts = nests[n]
+                    nests[n] = (dom, rank, stmts[:k] + stmts[k + 1:])
+                    hit = (kp, KProg(kp.slots, kp.scalar_names, kp.ntemps, tuple(nests), kp.fused_names))
+                    self._alias_k[key] = hit
+                sd_fold = (tslot, spmv_dot)
+                kp = hit[1]
         h, nred = self.kernel_handle(kp)
         scal = self._scalars(task.scalars)
         nslots = len(kp.slots)
@@ -963,6 +1031,10 @@ class Executor:
                 self._rec["pub"] = True
                 self._rec["counts"] = (c_int32 * self.world)(*counts)
         aliased = self._alias_candidates(kp, task)
+        if sd_fold is not None:
+            recorded = None
+            if self._rec is not None:
+                self._rec["ok"] = False
         if aliased:
             recorded = None  # copy-ins and rewritten kernels are planned per launch
             if self._rec is not None:
@@ -1012,6 +1084,24 @@ class Executor:
             if self._rec is not None:
                 self._rec["views"].append((views, [
                     (si, task.args[s.arg].store) for si, s in enumerate(kp.slots) if not s.local]))
+        if sd_fold is not None:
+            # the removed statement's p.q: each point's SpMV partials folded in a fixed order into
+            # a total, then target += total in point order (executor.py:193-195)
+            tslot, sd = sd_fold
+            tot = c_uint64()
+            check(self.lib.dk_scratch_alloc(8, byref(tot)))
+            tv0 = dk_view()
+            tv0.ptr, tv0.rank, tv0.dtype = tot.value, 0, DK_F64
+            a = task.args[kp.slots[tslot].arg]
+            r = self.stores[a.store]
+            for i in sorted(mine):
+                _rect, parts, nparts = sd["pts"][i]
+                check(self.lib.dk_memset_zero(tot.value, 8))
+                check(self.lib.dk_accum(byref(tv0), parts, 0, 1, nparts))
+                tv = self.view(r, rects[i][kp.slots[tslot].arg])
+                check(self.lib.dk_accum(byref(tv), tot.value, 0, 1, 1))
+            check(self.lib.dk_scratch_free(tot.value))
+            self.spmv_dot_stats["consumed"] += 1
         if use_totals:
             block = maxp * nred
             gathered = totals + 8 * block  # [world][maxp][nred] after the allgather
@@ -1134,6 +1224,7 @@ class Executor:
             tb = c_uint64()
             check(self.lib.dk_scratch_alloc(8 * block * (self.world + 1), byref(tb)))
             check(self.lib.dk_memset_zero(tb.value, 8 * block * (self.world + 1)))
+        sd_pts = {}
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * max(n, 1))()
             for j, a in enumerate(task.args):
@@ -1158,11 +1249,25 @@ class Executor:
                     scratch.append(p)
             if scratch and self._rec is not None:
                 self._rec["ok"] = False
-            check(self.lib.dk_builtin(kind, views, n, wflags))
+            if (self.fuse_spmv_dot and task.kind == "SPMV_CSR" and not scratch and not arenas
+                    and len(rects[i][4][0]) == 1 and self.shape(task.args[3].store) == self.shape(task.args[4].store)):
+                # opt-in epilogue: the SpMV also emits partials of x_tile . y for the next window
+                parts = c_uint64()
+                check(self.lib.dk_scratch_alloc(8 * 4096, byref(parts)))
+                np_ = c_int()
+                check(self.lib.dk_spmv_csr_dot(views, parts.value, rects[i][4][0][0], byref(np_)))
+                sd_pts[i] = (rects[i][4], parts.value, np_.value)
+                if self._rec is not None:
+                    self._rec["ok"] = False
+            else:
+                check(self.lib.dk_builtin(kind, views, n, wflags))
             for p in scratch:
                 check(self.lib.dk_scratch_free(p))
             if self._rec is not None:
                 self._rec["views"].append(((views, [(j, a.store) for j, a in enumerate(task.args)]), n, wflags))
+        if sd_pts:
+            self._sd = {"x": task.args[3].store, "y": task.args[4].store, "pts": sd_pts}
+            self.spmv_dot_stats["spmv"] += 1
         if arenas:
             gathered = tb.value + 8 * block
             check(self.lib.dk_comm_allgather_f64(tb.value + 8 * block * self.rank, gathered, block))

@@ -94,6 +94,7 @@ _SIGS = {
     "dk_launch": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_uint64]),
     "dk_accum": (c_int, [POINTER(dk_view), c_uint64, c_int64, c_int64, c_int]),
     "dk_builtin": (c_int, [c_char_p, POINTER(dk_view), c_int, POINTER(c_int32)]),
+    "dk_spmv_csr_dot": (c_int, [POINTER(dk_view), c_uint64, c_int64, POINTER(c_int)]),
     "dk_comm_unique_id": (c_int, [POINTER(c_uint8)]),
     "dk_comm_init": (c_int, [c_int, c_int, POINTER(c_uint8)]),
     "dk_comm_destroy": (c_int, []),

@@ -390,6 +390,21 @@ class FakeLib:
             t[...] += arr[first + i * stride]
         return 0
 
+    def dk_spmv_csr_dot(self, views, parts, x_row0, nparts_ref):
+        from oracle.interp import spmv_csr_rows
+
+        v = [self._view(views[j]) for j in range(5)]
+        y = spmv_csr_rows(v[0], v[1], v[2], v[3])
+        v[4][...] = y.reshape(v[4].shape)
+        acc = 0.0
+        for i in range(y.size):
+            acc = acc + float(v[3].reshape(-1)[x_row0 + i]) * float(y[i])
+        pb, off = self._resolve(parts)
+        pb[off:].view(np.float64)[0] = acc
+        _set(nparts_ref, 1)
+        self.launches += 1
+        return 0
+
     def dk_builtin(self, kind, views, n, writes):
         from paper_2406_18109_b200.ir import ArgDesc, NONE_PART, TaskDesc
 

@@ -207,3 +207,28 @@ def test_graph_segments_replay_identical_launches(monkeypatch):
         if name == "blackscholes_chain":
             gs = gpu.executor.graph_stats
             assert gs["captures"] >= 1 and gs["graph_launches"] >= 2, gs
+
+
+@pytest.mark.parametrize("name", ["cg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused", "pcg_csr_8x8_k2/fused"])
+def test_spmv_dot_epilogue_matches_reference(name):
+    """DK_FUSE_SPMV_DOT: the SpMV emits p.q partials and the [DOT, DOT] window drops that reduction;
+    heaps match the reference within rtol 1e-12 (the only change is the summation order of p.q)."""
+    from conftest import load_golden
+    from fakedev import FakeLib
+
+    from paper_2406_18109_b200.executor import Executor
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    case = {c["name"]: c for c in load_golden("bench_small.json.gz")}[name]
+    tr = PlanTrace.from_json(case["trace"])
+    ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes, lib=FakeLib(0, 1, device_model=True),
+                  fuse_spmv_dot=True)
+    for kind, ev in tr.events:
+        if kind == "exec":
+            ex.execute(ev.task, ev.kernel, ev.temp_positions)
+        elif kind == "free":
+            ex.free(ev)
+    assert ex.spmv_dot_stats["consumed"] >= 3 and ex.spmv_dot_stats["consumed"] == ex.spmv_dot_stats["spmv"]
+    for s, want in golden_arrays(case).items():
+        got = ex.get(s)
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(want)))))

@@ -71,13 +71,14 @@ def _red_targets(step, shapes):
     return sorted({a.store for a in step.task.args if a.reduces and shapes[a.store] == ()})
 
 
-def _run(tr, iters, lockstep):
+def _run(tr, iters, lockstep, fuse_spmv_dot=False):
     """Device replay of the first ``iters`` iterations; with ``lockstep`` the oracle runs window by
     window beside it and takes the device's reduction results.  Returns (executor, oracle heap, rank-0 log)."""
     from oracle.interp import OracleHeap, execute_step, parallel
     from paper_2406_18109_b200.executor import Executor
 
-    ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes, device=0)
+    ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes, device=0,
+                  fuse_spmv_dot=fuse_spmv_dot)
     oh = OracleHeap(tr.shapes, tr.seed, tr.init) if lockstep else None
     worst = 0.0
     with parallel(WORKERS):
@@ -168,12 +169,15 @@ def test_cg_lockstep_bit_identical(name, iters):
         ex.close()
 
 
-@pytest.mark.parametrize("name", ["cg_fused_n1", "pcg_fused_n1"])
-def test_cg_free_running_residual_history(name):
-    """Device and oracle each on their own: rs_new / rz_new histories within 1e-10 relative."""
+@pytest.mark.parametrize("name,fuse", [("cg_fused_n1", False), ("pcg_fused_n1", False), ("cg_fused_n1", True)])
+def test_cg_free_running_residual_history(name, fuse):
+    """Device and oracle each on their own: rs_new / rz_new histories within 1e-10 relative
+    (``fuse``: with the opt-in SpMV + partial-dot epilogue, DK_FUSE_SPMV_DOT)."""
     tr = _trace(name)
     t0 = time.time()
-    ex, _, _ = _run(tr, ITERS, lockstep=False)
+    ex, _, _ = _run(tr, ITERS, lockstep=False, fuse_spmv_dot=fuse)
+    if fuse:
+        assert ex.spmv_dot_stats["consumed"] >= ITERS - 1
     try:
         oh = _oracle(tr, ITERS)
         alive = _alive(ex, oh)

@@ -287,3 +287,26 @@ def test_device_pcg64_rejection_path(Executor):
         assert r.pcg is not None and len(r.pcg[1]) >= 1
     finally:
         ex.close()
+
+
+def test_spmv_dot_epilogue_golden(Executor, bench_cases):
+    """DK_FUSE_SPMV_DOT on the reference's CG / PCG golden cases: the SpMV kernel's partial-dot
+    epilogue replaces the window's p.q reduction; heaps within rtol 1e-12 of the reference."""
+    from paper_2406_18109_b200.executor import replay
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    n = 0
+    for case in bench_cases:
+        if not case["name"].startswith(("cg_csr", "pcg_csr")) or not case["name"].endswith("/fused"):
+            continue
+        trace = PlanTrace.from_json(case["trace"])
+        ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, device=0,
+                      fuse_spmv_dot=True)
+        try:
+            replay(ex, trace.events)
+            assert ex.spmv_dot_stats["consumed"] >= 3
+            _compare(case["name"], {s: ex.get(s) for s in trace.live}, golden_arrays(case), False)
+            n += 1
+        finally:
+            ex.close()
+    assert n >= 3
