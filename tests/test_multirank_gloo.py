@@ -165,3 +165,25 @@ def test_fuzz_corpus_two_ranks_match_reference():
     res = _run(names)
     bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
+
+
+def _k8_traces():
+    import gzip
+    import json
+
+    from conftest import GOLDEN
+
+    with gzip.open(os.path.join(GOLDEN, "plans_k8.json.gz"), "rt") as f:
+        return json.load(f)["traces"]
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_eight_point_plans_on_four_and_eight_ranks(world):
+    """Stencil bands, CSR CG and Jacobi-PCG with 8 launch points (the 8-GPU plan shape) on 4 and 8
+    ranks -- two and one points per rank; halos, replicated reads and point-order folds against the
+    oracle, byte for byte; with the peer-board reductions at world 8."""
+    traces = _k8_traces()
+    res = _run(traces, world=world, p2p=(world == 8))
+    bad = [b for _, bs, *_ in res for b in bs]
+    assert not bad, bad[:10]
+    assert all(r[2] > 0 for r in res), res

@@ -55,10 +55,31 @@ def main():
     if "--large-only" in sys.argv:
         large()
         return
+    if "--multirank-only" in sys.argv:
+        multirank()
+        return
     if "--medium-only" not in sys.argv:
         full_size()
     medium()
     large()
+    multirank()
+
+
+def multirank():
+    """Eight-point plans for the world-4 / world-8 gloo tests (tests/test_multirank_gloo.py):
+    one or two launch points per rank, compared with the oracle there."""
+    out = []
+    for name, gen, iters in [
+        ("stencil_bands_n4_k8", lambda it: W.stencil_bands(4, 8, it), 3),
+        ("cg_csr_8x16_k8", lambda it: W.cg_csr(8, 16, 8, it), 4),
+        ("pcg_csr_8x16_k8", lambda it: W.pcg_csr(8, 16, 8, it), 4),
+    ]:
+        for fused in (True, False):
+            tr = capture(f"{name}/{'fused' if fused else 'unfused'}", gen, iters, fused)
+            out.append(tr.to_json())
+    with gzip.open(os.path.join(REPO, "tests", "golden", "plans_k8.json.gz"), "wt", compresslevel=9) as f:
+        json.dump({"format": "dk-plans-1", "traces": out}, f, separators=(",", ":"))
+    print("k8 traces:", len(out))
 
 
 def large():

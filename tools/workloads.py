@@ -209,3 +209,69 @@ def pcg_csr(nx: int, ny: int, k: int, iters: int):
         b.drop(rz_old)
         b.flush()
     return b.events, b.init, b.dtypes
+
+
+# --------------------------------------------------------------------------
+# JSON-lines: the reference's own trace format (trace.py:73-192)
+# --------------------------------------------------------------------------
+# The new workloads are written with the reference's printer and read with its
+# parser, so ``diffusekit analyze / canon / run`` inspect them unchanged.  Their
+# initial contents (zero reduction targets, CSR tiles, seeded uniform vectors)
+# and backend dtype overrides travel as extra keys on the ``create_store`` line
+# ("init", "dtype"): the reference parser reads only the keys it knows
+# (trace.py:128-137), so the file stays a valid reference trace.
+
+
+def write_jsonl(events, init=None, dtypes=None) -> str:
+    import json
+
+    from diffusekit.trace import CreateStore, event_to_json
+
+    init, dtypes = dict(init or {}), dict(dtypes or {})
+    lines = []
+    for ev in events:
+        obj = event_to_json(ev)
+        if isinstance(ev, CreateStore):
+            if ev.id in init:
+                obj["init"] = init[ev.id]
+            if ev.id in dtypes:
+                obj["dtype"] = dtypes[ev.id]
+        lines.append(json.dumps(obj))
+    return "\n".join(lines) + "\n"
+
+
+def read_jsonl(text: str):
+    """(events, init, dtypes): the reference parser's events plus the harness annotations."""
+    import json
+
+    from diffusekit.trace import parse_trace
+
+    events = parse_trace(text)
+    init, dtypes = {}, {}
+    for raw in text.splitlines():
+        raw = raw.strip()
+        if not raw:
+            continue
+        obj = json.loads(raw)
+        if obj.get("event") == "create_store":
+            if "init" in obj:
+                init[int(obj["id"])] = obj["init"]
+            if "dtype" in obj:
+                dtypes[int(obj["id"])] = obj["dtype"]
+    return events, init, dtypes
+
+
+def cli_main():
+    """python tools/workloads.py {stencil|cg|pcg|bs} [size args] > trace.jsonl"""
+    import sys
+
+    kind, *a = sys.argv[1:]
+    a = [int(v) for v in a]
+    gen = {"stencil": stencil_bands, "cg": cg_csr, "pcg": pcg_csr, "bs": blackscholes}[kind]
+    out = gen(*a)
+    events, init, dtypes = (out + ({},))[:3] if len(out) == 2 else out
+    sys.stdout.write(write_jsonl(events, init, dtypes))
+
+
+if __name__ == "__main__":
+    cli_main()
