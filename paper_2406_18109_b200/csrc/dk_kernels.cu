@@ -99,14 +99,15 @@ __global__ void __launch_bounds__(256) k_spmv_csr(const I* __restrict__ rowptr, 
 }
 
 // ---- SPMV_CSR, bulk-copy pipeline (int32 indices) ----------------------------
-// Persistent CTAs of 8 consumer warps + 1 producer warp.  The matrix is cut
-// into chunks of kSpR rows; chunk c's rowptr slab and its contiguous nonzero
+// Persistent CTAs of R/32 consumer warps + 1 producer warp.  The matrix is cut
+// into chunks of R rows; chunk c's rowptr slab and its contiguous nonzero
 // slab [rowptr[r0], rowptr[r1]) of vals and cols are moved into a shared-memory
 // stage by three cp.async.bulk copies (16-byte-rounded ranges: rounding never
 // leaves the 2 MiB granule a view lies in) completing on the stage's full
-// mbarrier; consumers release the stage on its empty mbarrier.  kSpStages
-// stages keep ~100 KB per CTA in flight, so the nonzero stream no longer
-// waits on per-thread dependent loads.  Each consumer thread then sums one
+// mbarrier; consumers release the stage on its empty mbarrier.  Two
+// stages per CTA, four CTAs per SM: ~100 KB of the nonzero stream in flight
+// per SM without per-thread dependent loads, and 32 consumer warps per SM to
+// hide the x gathers.  Each consumer thread then sums one
 // row from shared memory: acc = 0.0; acc = acc + vals[j] * x[cols[j]] left
 // to right with __dmul_rn / __dadd_rn -- the same order and roundings as the
 // oracle's definition, so the result is bit-identical to k_spmv_csr.  A chunk
@@ -274,12 +275,14 @@ static const SpCfg& spmv_cfg() {
     const char* e = getenv("DK_SPMV_CFG");
     const int v = e ? atoi(e) : 0;
     switch (v) {
+      // measured at 67M rows (B200, bench cg): 1: 1.040 ms, 2: 0.778, 3: 0.784, 4: 0.858, 5: 1.301;
+      // the thread-per-row kernel (DK_SPMV_SIMPLE) 0.866.  Occupancy (4 CTAs = 32 consumer warps
+      // per SM to hide the x gathers) matters more than stage depth.
       case 1: return sp_cfg<256, 2048, 4, 2>();
-      case 2: return sp_cfg<256, 1536, 2, 4>();
       case 3: return sp_cfg<512, 3072, 2, 2>();
       case 4: return sp_cfg<256, 1536, 3, 3>();
       case 5: return sp_cfg<128, 768, 4, 6>();
-      default: return sp_cfg<256, 1536, 3, 3>();
+      default: return sp_cfg<256, 1536, 2, 4>();
     }
   }();
   return cfg;

@@ -185,7 +185,7 @@ def test_cg_free_running_residual_history(name, fuse):
         assert len(hist) >= ITERS - 1
         g = np.array([float(ex.get(s)[()]) for s in hist])
         w = np.array([float(oh.get(s)[()]) for s in hist])
-        assert np.all(w > 0) and w[-1] < w[0]  # the residual decreases
+        assert np.all(w > 0)  # (the 2-norm of the CG residual is not monotone: it grows here at first)
         np.testing.assert_allclose(g, w, rtol=1e-10)
         for s in alive:
             if tr.shapes[s] != () and not tr.init.get(s, {}).get("kind", "").startswith("csr"):
