@@ -841,7 +841,14 @@ def run_ours(args):
             per_rank = gather_all(torch, world, ms / (steps or args.steps))
             host_rank = gather_all(torch, world, measure.host_ms / (steps or args.steps))
             ms = reduce_max(torch, world, ms)
+            per_exec_ranks = None
+            if world > 1 and dom is not None:
+                import torch.distributed as dist
+
+                per_exec_ranks = [None] * world
+                dist.all_gather_object(per_exec_ranks, dom["per_exec_ms"])
             res = {"ms": ms, "ranks_ms_per_step": per_rank, "host_ms_per_step": host_rank, "launches": launches,
+                   "per_exec_ms_ranks": per_exec_ranks,
                    "dom": dom, "it_bytes": it_bytes, "stats": vars(ex.stats),
                    "jit": ex.jit_stats(), "check": check}
             if with_e2e:
@@ -905,6 +912,7 @@ def run_ours(args):
         "roofline": roof,
         "hbm_gbs_step": round(main["it_bytes"] / (main["ms"] / K / 1e3) / 1e9, 1),
         "per_exec_ms": dom["per_exec_ms"] if dom else None,
+        "per_exec_ms_ranks": main["per_exec_ms_ranks"],
         "gpu_launches": main["launches"],
         "ranks_ms_per_step": main["ranks_ms_per_step"],
         "host_enqueue_ms_per_step": main["host_ms_per_step"],
@@ -938,6 +946,7 @@ def run_ours(args):
                     "unfused_iter_s": round(world * K / (u["ms"] / 1e3), 3),
                     "fused_over_unfused": round(u["ms"] / f["ms"], 3),
                     "fused_ranks_ms_per_step": f["ranks_ms_per_step"],
+                    "fused_per_exec_ms_ranks": f["per_exec_ms_ranks"],
                     "fused_host_enqueue_ms_per_step": f["host_ms_per_step"],
                     "fused_hbm_gbs_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9, 1),
                     "fused_hbm_frac_step": round(f["it_bytes"] / (f["ms"] / K / 1e3) / 1e9 / hbm_peak, 4),

@@ -150,6 +150,7 @@ int dk_comm_exchange(int n, const int64_t* sids, const int32_t* peers, const int
   return guard([&] {
     require_init();
     if (n <= 0) return;
+    NvtxRange nv("dk_comm_exchange", n);
     ncclComm_t c = comm();
     cudaStream_t s = st().stream;
     std::vector<RectView> rvs(n);
@@ -264,6 +265,7 @@ int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered) {
   return guard([&] {
     require_init();
     require_not_capturing("dk_p2p_wait");
+    NvtxRange nv("dk_p2p_wait", slot);
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
     if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);

@@ -14,9 +14,29 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dk_b200.h"
 
 namespace dk {
+
+// NVTX range around each C-ABI launch entry point (named by kind, payload = kernel
+// handle or launch count): visible to Nsight tools, a no-op without one attached.
+struct NvtxRange {
+  NvtxRange(const char* name, int64_t payload) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    a.payloadType = NVTX_PAYLOAD_TYPE_INT64;
+    a.payload.llValue = payload;
+    nvtxRangePushEx(&a);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct Error : std::runtime_error {
   int code;

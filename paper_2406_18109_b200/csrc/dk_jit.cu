@@ -1960,6 +1960,7 @@ int dk_launch(int64_t handle, const dk_view* views, int nviews, const double* sc
               uint64_t totals) {
   return guard([&] {
     require_init();
+    NvtxRange nv("dk_launch", handle);
     launch(kernel_of(handle), views, nviews, scalars, nscalars, totals);
   });
 }
@@ -1969,6 +1970,7 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
   return guard([&] {
     require_init();
     require_not_capturing("dk_launch_pub (board slots are epoch-numbered)");
+    NvtxRange nv("dk_launch_pub", handle);
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
     if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);

@@ -520,6 +520,7 @@ int dk_accum(const dk_view* target, uint64_t vals, int64_t first, int64_t stride
 int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t* writes) {
   return guard([&] {
     require_init();
+    NvtxRange nv(kind, st().launches);
     launch_builtin(kind, views, nviews, writes, st().stream);
   });
 }
@@ -527,6 +528,7 @@ int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t
 int dk_spmv_csr_dot(const dk_view* views, uint64_t parts, int64_t x_row0, int* nparts) {
   return guard([&] {
     require_init();
+    NvtxRange nv("SPMV_CSR+dot", st().launches);
     *nparts = launch_spmv_csr_dot(views, (double*)parts, x_row0, st().stream);
   });
 }
