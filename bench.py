@@ -428,8 +428,9 @@ def result_check(ex, trace, wl, its, nxt, torch, world):
         vec = {}
         for name, sid in (("x", x_sid), ("r", r_sid), ("aux", 7 if wl == "cg" else 6)):
             vec[name] = ex.download_local(sid, np.empty(trace.shapes[sid]), rect)[lo:hi]
-        red_win = [e for e in execs if any(a.store == r_sid and a.writes for a in e.task.args)]
-        tgt = [a.store for a in red_win[-1].task.args if a.reduces and trace.shapes[a.store] == ()][-1]
+        # rs_new / rz_new: the first reduction at or after the last window that writes r
+        last_w = max(k for k, e in enumerate(execs) if any(a.store == r_sid and a.writes for a in e.task.args))
+        tgt = next(a.store for e in execs[last_w:] for a in e.task.args if a.reduces and trace.shapes[a.store] == ())
         if wl == "cg":
             out["resid_eq_minus_r"] = bool(np.array_equal(vec["aux"], -vec["r"]))
             dot = _allsum(torch, world, sum(_rows_parallel(lambda a, b: float(np.dot(vec["r"][a:b], vec["r"][a:b])), hi - lo)))

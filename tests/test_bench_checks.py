@@ -41,7 +41,8 @@ def _setup(bench, name, n_its):
 
 @pytest.mark.parametrize("wl,name", [("stencil", "stencil_fused_cpu"), ("cg", "cg_fused_cpu"),
                                      ("pcg", "pcg_fused_cpu"), ("stencil", "stencil_unfused_cpu"),
-                                     ("bs", "bs_fused_c1")])
+                                     ("cg", "cg_unfused_cpu"), ("pcg", "pcg_unfused_cpu"),
+                                     ("bs", "bs_fused_c1"), ("bs", "bs_unfused_c1")])
 def test_result_check_passes(bench, wl, name):
     ex, tr, its = _setup(bench, name, 4)
     out = bench.result_check(ex, tr, wl, its, 4, None, 1)
