@@ -175,14 +175,19 @@ int dk_comm_barrier(void);
 #define DK_P2P_RED 32
 /* collective (after dk_comm_init): *enabled = 1 iff every rank mapped every peer's board */
 int dk_p2p_init(int* enabled);
-/* dk_launch with totals published to all ranks' boards: ring slot `slot`,
- * `point` = ordinal of this launch point among the calling rank's points */
+/* dk_launch with totals published to all ranks' boards for reduction number
+ * `epoch` (0, 1, 2, ... in the same order on every rank; ring slot epoch mod
+ * DK_P2P_SLOTS), `point` = ordinal of this launch point among the calling
+ * rank's points.  The flag raised in each board holds the epoch's tag
+ * (epoch mod 2^31, + 1), so a consumer can tell this epoch's totals from an
+ * older or newer use of the slot. */
 int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
-                  int slot, int point);
+                  int64_t epoch, int point);
 /* stream-ordered wait until counts[q] points of every rank q have published
- * into this rank's slot (flags consumed); *gathered = the slot's totals,
- * layout [world][DK_P2P_POINTS][nred] as dk_accum's `vals` */
-int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered);
+ * epoch `epoch` into this rank's board (flags consumed); a flag holding any
+ * other epoch's tag is a protocol violation and traps; *gathered = the slot's
+ * totals, layout [world][DK_P2P_POINTS][nred] as dk_accum's `vals` */
+int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered);
 
 #ifdef __cplusplus
 }

@@ -75,7 +75,7 @@ struct P2PCounts {
   int c[kP2PWMax];
 };
 
-__global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world) {
+__global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world, unsigned tag) {
   const int q = threadIdx.x / DK_P2P_POINTS, j = threadIdx.x % DK_P2P_POINTS;
   if (q < world && j < counts.c[q]) {
     unsigned int* f = flags + q * DK_P2P_POINTS + j;
@@ -84,7 +84,12 @@ __global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world) {
     for (;;) {
       unsigned int v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if (v) break;
+      if (v == tag) break;
+      if (v != 0u) {
+        // another epoch's publish in this slot: the ring invariant is broken
+        printf("dk_p2p_wait: rank %d point %d flag holds tag %u, expected %u\n", q, j, v, tag);
+        __trap();
+      }
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 10000000000ull) __trap();
       __nanosleep(64);
@@ -261,21 +266,23 @@ int dk_p2p_init(int* enabled) {
   });
 }
 
-int dk_p2p_wait(int slot, const int32_t* counts, uint64_t* gathered) {
+int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered) {
   return guard([&] {
     require_init();
     require_not_capturing("dk_p2p_wait");
-    NvtxRange nv("dk_p2p_wait", slot);
+    NvtxRange nv("dk_p2p_wait", epoch);
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
-    if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);
+    if (epoch < 0) fail(DK_ERR_ARG, "negative reduction epoch");
+    const int slot = (int)(epoch % DK_P2P_SLOTS);
     P2PCounts pc = {};
     for (int q = 0; q < S.world; ++q) {
       if (counts[q] < 0 || counts[q] > DK_P2P_POINTS) fail(DK_ERR_ARG, "rank %d publishes %d points", q, counts[q]);
       pc.c[q] = counts[q];
     }
     char* b = (char*)S.board;
-    k_p2p_wait<<<1, kP2PWMax * DK_P2P_POINTS, 0, S.stream>>>((unsigned int*)(b + p2p_flag_off(slot)), pc, S.world);
+    k_p2p_wait<<<1, kP2PWMax * DK_P2P_POINTS, 0, S.stream>>>((unsigned int*)(b + p2p_flag_off(slot)), pc, S.world,
+                                                            p2p_tag(epoch));
     DK_CUDA(cudaGetLastError());
     S.launches++;
     *gathered = (uint64_t)(b + p2p_data_off(slot));

@@ -130,6 +130,8 @@ constexpr size_t kP2PFlagBytes = (size_t)kP2PWMax * DK_P2P_POINTS * 4;
 inline size_t p2p_data_off(int slot) { return (size_t)slot * kP2PSlotBytes; }
 inline size_t p2p_flag_off(int slot) { return DK_P2P_SLOTS * kP2PSlotBytes + (size_t)slot * kP2PFlagBytes; }
 constexpr size_t kP2PBoardBytes = DK_P2P_SLOTS * (kP2PSlotBytes + kP2PFlagBytes);
+// flag value published for a reduction epoch (0 means "not published")
+inline unsigned p2p_tag(int64_t epoch) { return (unsigned)(epoch & 0x7fffffff) + 1u; }
 
 State& st();
 void require_init();

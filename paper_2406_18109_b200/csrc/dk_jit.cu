@@ -234,6 +234,7 @@ struct DkPub {
   uint64_t dst[8];   // the same block in every rank's board
   uint64_t flag[8];  // the point's flag in every rank's board
   int64_t n, nred;   // ranks to publish to (0: no publish), doubles per block
+  int64_t tag;       // flag value: the reduction epoch's tag (never 0)
 };
 // union region of a register-swept K3 nest
 struct DkUni {
@@ -241,7 +242,7 @@ struct DkUni {
   int64_t rs, cols, rows;
 };
 static_assert(sizeof(DkHdr) == 8 * 11, "DkHdr layout");
-static_assert(sizeof(DkPub) == 8 * 19, "DkPub layout");
+static_assert(sizeof(DkPub) == 8 * 20, "DkPub layout");
 static_assert(sizeof(DkSite) == 48, "DkSite layout");
 static_assert(sizeof(dk_view) == 80, "dk_view layout");
 
@@ -603,7 +604,7 @@ typedef unsigned int uint32_t;
 struct dk_view { uint64_t ptr; int32_t rank; int32_t dtype; int64_t ext[4]; int64_t stride[4]; };
 struct DkHdr { int64_t ext[4]; int64_t nrows, ninner, nelem; uint64_t red_part, red_ticket, red_totals; int64_t red_mode; };
 struct DkSite { uint64_t p; int64_t st[3]; int64_t sti; int64_t mode; };
-struct DkPub { uint64_t src; uint64_t dst[8]; uint64_t flag[8]; int64_t n, nred; };
+struct DkPub { uint64_t src; uint64_t dst[8]; uint64_t flag[8]; int64_t n, nred, tag; };
 struct DkUni { uint64_t base; int64_t rs, cols, rows; };
 // element pair q of row r of a K3 union region (16-byte aligned base, even row stride)
 __device__ __forceinline__ double2 dk_ldu(const DkUni& u, int64_t r, int64_t q) {
@@ -1448,7 +1449,7 @@ class Gen {
         << " for (int k = 0; k < (int)P.pub.nred; ++k) d[k] = src[k]; }\n"
         << "      __threadfence_system();\n"
         << "      for (int q = 0; q < (int)P.pub.n; ++q)"
-        << " asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(P.pub.flag[q]), \"r\"(1u) : \"memory\");\n"
+        << " asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(P.pub.flag[q]), \"r\"((unsigned)P.pub.tag) : \"memory\");\n"
         << "    }\n";
     }
   }
@@ -1965,15 +1966,16 @@ int dk_launch(int64_t handle, const dk_view* views, int nviews, const double* sc
   });
 }
 
-int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars, int slot,
-                  int point) {
+int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+                  int64_t epoch, int point) {
   return guard([&] {
     require_init();
     require_not_capturing("dk_launch_pub (board slots are epoch-numbered)");
     NvtxRange nv("dk_launch_pub", handle);
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
-    if (slot < 0 || slot >= DK_P2P_SLOTS) fail(DK_ERR_ARG, "board slot %d out of range", slot);
+    if (epoch < 0) fail(DK_ERR_ARG, "negative reduction epoch");
+    const int slot = (int)(epoch % DK_P2P_SLOTS);
     if (point < 0 || point >= DK_P2P_POINTS) fail(DK_ERR_ARG, "point %d exceeds the board's %d points per rank", point, DK_P2P_POINTS);
     KernelObj& k = kernel_of(handle);
     const int nred = k.prog.nreduce;
@@ -1982,6 +1984,7 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
     DkPub pub = {};
     pub.n = S.world;
     pub.nred = nred;
+    pub.tag = p2p_tag(epoch);
     pub.src = (uint64_t)S.board + p2p_data_off(slot) + off;
     for (int q = 0; q < S.world; ++q) {
       pub.dst[q] = S.peer_board[q] + p2p_data_off(slot) + off;

@@ -703,12 +703,12 @@ class Executor:
             scal = self._scalars(task.scalars)
             ns, nsl = len(task.scalars), len(kp.slots)
             if hit["pub"]:
-                slot = self._p2p_epoch % runtime.P2P_SLOTS
+                epoch = self._p2p_epoch
                 self._p2p_epoch += 1
                 for sir, cv in enumerate(hit["views"]):
-                    check(self.lib.dk_launch_pub(h, self._rebind(cv, bases), nsl, scal, ns, slot, sir))
+                    check(self.lib.dk_launch_pub(h, self._rebind(cv, bases), nsl, scal, ns, epoch, sir))
                 g = c_uint64()
-                check(self.lib.dk_p2p_wait(slot, hit["counts"], byref(g)))
+                check(self.lib.dk_p2p_wait(epoch, hit["counts"], byref(g)))
                 for cv, first, stride, nv in hit["fold"]:
                     check(self.lib.dk_accum(byref(self._rebind(cv, bases)), g.value, first, stride, nv))
                 self.stats.p2p_folds += 1
@@ -1002,7 +1002,7 @@ class Executor:
         V = len(prank)
         totals = 0
         maxp = 0
-        pub_slot = -1
+        pub_slot = -1  # reduction epoch of a peer-board launch (-1: none)
         if use_totals:
             counts = [0] * self.world
             for q in prank:
@@ -1013,7 +1013,7 @@ class Executor:
             # DK_P2P_SLOTS epochs behind its peers (their publishes would overwrite
             # a slot it has not folded yet) -- such launches take the NCCL gather
             if self._p2p and not isolated and min(counts) >= 1 and maxp <= runtime.P2P_POINTS and nred <= runtime.P2P_RED:
-                pub_slot = self._p2p_epoch % runtime.P2P_SLOTS
+                pub_slot = self._p2p_epoch  # the reduction epoch (board slot = epoch mod P2P_SLOTS)
                 self._p2p_epoch += 1
                 use_totals = False
         if use_totals:

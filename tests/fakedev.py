@@ -484,21 +484,23 @@ class FakeLib:
         _set(ref, 1 if getattr(self, "p2p_enabled", False) else 0)
         return 0
 
-    def dk_launch_pub(self, h, views, nviews, scalars, nscal, slot, point):
+    def dk_launch_pub(self, h, views, nviews, scalars, nscal, epoch, point):
         from paper_2406_18109_b200 import runtime as rt
 
+        slot = epoch % rt.P2P_SLOTS
         nred = sum(1 for _, _, sts in self.kernels[h].nests for st in sts if st[0] == "reduce")
         assert 0 <= point < rt.P2P_POINTS and 0 < nred <= rt.P2P_RED
         off = 8 * (slot * self.p2p_slot_doubles + nred * (self.rank * rt.P2P_POINTS + point))
         self.p2p_nred[slot] = nred
         return self.dk_launch(h, views, nviews, scalars, nscal, self.board_ptr + off)
 
-    def dk_p2p_wait(self, slot, counts, ref):
+    def dk_p2p_wait(self, epoch, counts, ref):
         import torch
         import torch.distributed as dist
 
         from paper_2406_18109_b200 import runtime as rt
 
+        slot = epoch % rt.P2P_SLOTS
         n = self.p2p_slot_doubles
         mine = self.allocs[self.board][8 * slot * n : 8 * (slot + 1) * n].view(np.float64)
         t = torch.from_numpy(np.concatenate([mine, [float(self.p2p_nred.pop(slot, 0))]]))
