@@ -189,6 +189,21 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
  * totals, layout [world][DK_P2P_POINTS][nred] as dk_accum's `vals` */
 int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered);
 
+/* Halo / replicated-read moves over peer memory instead of NCCL send/recv
+ * (same arguments as dk_comm_exchange).  Each rank's board also holds a
+ * mailbox per (source rank, parity) of DK_P2P_MAIL_BYTES: one kernel packs
+ * this rank's send rects straight into the receivers' mailboxes over NVLink
+ * and raises a flag there (tag of the pair's exchange epoch); its receive CTAs
+ * wait for the senders' flags, unpack into the store rects and acknowledge,
+ * so a sender reuses a mailbox parity only after the receiver consumed it.
+ * `epochs[q]` = number of earlier exchanges between this rank and rank q (the
+ * same count on both sides: the plan is replicated).  Fails with
+ * DK_ERR_UNSUPPORTED if one pair's bytes exceed a mailbox; the caller then
+ * uses dk_comm_exchange (the decision is the same on both ranks). */
+#define DK_P2P_MAIL_BYTES (1 << 20)
+int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs, const int64_t* los,
+                    const int64_t* his, const int64_t* epochs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -99,11 +99,181 @@ __global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world, uns
   __threadfence_system();
 }
 
+// ---- halo moves over peer memory (dk_p2p_exchange) ----------------------------
+// One CTA per (peer, direction).  A send CTA waits for the receiver's ack of
+// the exchange two epochs back on this mailbox parity, copies its rects into
+// the receiver's mailbox [me][parity] (peer stores over NVLink), then thread 0
+// publishes the epoch's tag into the receiver's mail flag with release
+// semantics at system scope.  A receive CTA waits for that tag (acquire),
+// copies the mailbox into its store rects and acks into the sender's board.
+// A flag or ack holding an unexpected nonzero tag traps; 10 s without
+// progress traps (never a hang).
+constexpr int kXMaxItems = 8;
+struct XItem {
+  dk_view v;     // store rect (8- or 4-byte elements)
+  int64_t off;   // byte offset inside the mailbox
+  int64_t count; // elements
+};
+struct XCta {
+  int dir;            // 0 send, 1 recv
+  int nitems;
+  unsigned tag, prev; // this epoch's tag; the ack to wait for before sending (0: none)
+  uint64_t mail;      // send: receiver's mailbox base; recv: my mailbox base
+  uint64_t flag;      // send: receiver's mail flag; recv: my mail flag
+  uint64_t ack;       // send: my ack flag (written by the receiver); recv: the sender's ack flag
+  XItem item[kXMaxItems];
+};
+struct XArgs {
+  int ncta;
+  XCta cta[2 * kP2PWMax];
+};
+static_assert(sizeof(XArgs) < 32000, "kernel parameter block");
+
+__device__ __forceinline__ void x_wait(const unsigned int* f, unsigned tag, const char* what, int cta) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (v == tag) return;
+    if (v != 0u && what[0] == 'm') {  // a mail flag from another epoch
+      printf("dk_p2p_exchange: cta %d mail flag holds tag %u, expected %u\n", cta, v, tag);
+      __trap();
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 10000000000ull) {
+      printf("dk_p2p_exchange: cta %d timed out waiting for %s tag %u (last %u)\n", cta, what, tag, v);
+      __trap();
+    }
+    __nanosleep(32);
+  }
+}
+
+__device__ __forceinline__ int64_t x_elem_off(const dk_view& v, int64_t i) {
+  int64_t o = 0;
+  for (int d = v.rank - 1; d >= 0; --d) {
+    const int64_t e = v.ext[d];
+    o += (i % e) * v.stride[d];
+    i /= e;
+  }
+  return o;
+}
+
+__global__ void __launch_bounds__(1024) k_p2p_xchg(XArgs a) {
+  const XCta& c = a.cta[blockIdx.x];
+  if (c.dir == 0) {
+    if (c.prev && threadIdx.x == 0) x_wait((const unsigned int*)c.ack, c.prev, "ack", blockIdx.x);
+    __syncthreads();
+    for (int k = 0; k < c.nitems; ++k) {
+      const XItem& it = c.item[k];
+      const int es = it.v.dtype == DK_F64 ? 8 : 4;
+      char* dst = (char*)c.mail + it.off;
+      const char* src = (const char*)it.v.ptr;
+      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) {
+        const int64_t o = x_elem_off(it.v, i);
+        if (es == 8)
+          ((double*)dst)[i] = ((const double*)src)[o];
+        else
+          ((int*)dst)[i] = ((const int*)src)[o];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(c.flag), "r"(c.tag) : "memory");
+    }
+  } else {
+    if (threadIdx.x == 0) x_wait((const unsigned int*)c.flag, c.tag, "mail", blockIdx.x);
+    __syncthreads();
+    for (int k = 0; k < c.nitems; ++k) {
+      const XItem& it = c.item[k];
+      const int es = it.v.dtype == DK_F64 ? 8 : 4;
+      const char* src = (const char*)c.mail + it.off;
+      char* dst = (char*)it.v.ptr;
+      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) {
+        const int64_t o = x_elem_off(it.v, i);
+        if (es == 8)
+          ((double*)dst)[o] = ((const double*)src)[i];
+        else
+          ((int*)dst)[o] = ((const int*)src)[i];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *(volatile unsigned int*)c.flag = 0u;  // consumed (the sender's next write here is two epochs on)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(c.ack), "r"(c.tag) : "memory");
+    }
+  }
+}
+
 }  // namespace dk
 
 using namespace dk;
 
 extern "C" {
+
+int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs, const int64_t* los,
+                    const int64_t* his, const int64_t* epochs) {
+  return guard([&] {
+    require_init();
+    require_not_capturing("dk_p2p_exchange");
+    State& S = st();
+    if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer memory");
+    if (n <= 0) return;
+    NvtxRange nv("dk_p2p_exchange", n);
+    XArgs a = {};
+    int cta_of[2][kP2PWMax];
+    for (auto& r : cta_of)
+      for (int& x : r) x = -1;
+    for (int i = 0; i < n; ++i) {
+      const int q = peers[i], dir = dirs[i];
+      if (q < 0 || q >= S.world || q == S.rank) fail(DK_ERR_ARG, "bad peer %d", q);
+      Store& so = store_of(sids[i]);
+      RectView rv = rect_view(so, los + 4 * i, his + 4 * i);
+      if (rv.count == 0) continue;
+      int64_t last = rv.first;
+      for (int d = 0; d < so.rank; ++d) last += (rv.v.ext[d] - 1) * rv.v.stride[d];
+      store_ensure_bytes(so, (size_t)rv.first * so.esize, (size_t)(last + 1) * so.esize);
+      rv.v.ptr = (uint64_t)so.base + (uint64_t)rv.first * so.esize;
+      int& ci = cta_of[dir][q];
+      if (ci < 0) {
+        ci = a.ncta++;
+        XCta& c = a.cta[ci];
+        const int64_t e = epochs[q];
+        const int par = (int)(e & 1);
+        c.dir = dir;
+        c.tag = p2p_tag(e);
+        c.prev = e >= 2 ? p2p_tag(e - 2) : 0u;
+        if (dir == 0) {
+          c.mail = S.peer_board[q] + mail_data_off(S.rank, par);
+          c.flag = S.peer_board[q] + mail_flag_off(S.rank, par);
+          c.ack = (uint64_t)S.board + mail_ack_off(q, par);
+        } else {
+          c.mail = (uint64_t)S.board + mail_data_off(q, par);
+          c.flag = (uint64_t)S.board + mail_flag_off(q, par);
+          c.ack = S.peer_board[q] + mail_ack_off(S.rank, par);
+        }
+      }
+      XCta& c = a.cta[ci];
+      if (c.nitems >= kXMaxItems) fail(DK_ERR_UNSUPPORTED, "more than %d rects for one peer", kXMaxItems);
+      int64_t off = 0;
+      if (c.nitems) {
+        const XItem& pv = c.item[c.nitems - 1];
+        off = pv.off + ((pv.count * (pv.v.dtype == DK_F64 ? 8 : 4) + 15) & ~(int64_t)15);
+      }
+      if (off + rv.count * (int64_t)so.esize > (int64_t)kMailSlot)
+        fail(DK_ERR_UNSUPPORTED, "halo to rank %d exceeds the %d-byte mailbox", q, (int)kMailSlot);
+      XItem& it = c.item[c.nitems++];
+      it.v = rv.v;
+      it.off = off;
+      it.count = rv.count;
+    }
+    if (a.ncta == 0) return;
+    k_p2p_xchg<<<a.ncta, 1024, 0, S.stream>>>(a);
+    DK_CUDA(cudaGetLastError());
+    S.launches++;
+  });
+}
 
 int dk_comm_unique_id(uint8_t* out128) {
   return guard([&] {

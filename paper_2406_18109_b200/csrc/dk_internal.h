@@ -129,7 +129,19 @@ constexpr size_t kP2PSlotBytes = (size_t)kP2PWMax * DK_P2P_POINTS * DK_P2P_RED *
 constexpr size_t kP2PFlagBytes = (size_t)kP2PWMax * DK_P2P_POINTS * 4;
 inline size_t p2p_data_off(int slot) { return (size_t)slot * kP2PSlotBytes; }
 inline size_t p2p_flag_off(int slot) { return DK_P2P_SLOTS * kP2PSlotBytes + (size_t)slot * kP2PFlagBytes; }
-constexpr size_t kP2PBoardBytes = DK_P2P_SLOTS * (kP2PSlotBytes + kP2PFlagBytes);
+constexpr size_t kP2PRedBytes = DK_P2P_SLOTS * (kP2PSlotBytes + kP2PFlagBytes);
+// halo mailboxes after the reduction ring: data [src rank][parity], then mail
+// flags [src rank][parity] (raised by the sender), then ack flags [dst rank][parity]
+// (raised by the receiver in the sender's board)
+constexpr size_t kMailSlot = DK_P2P_MAIL_BYTES;
+inline size_t mail_data_off(int src, int par) { return kP2PRedBytes + (size_t)(src * 2 + par) * kMailSlot; }
+inline size_t mail_flag_off(int src, int par) {
+  return kP2PRedBytes + (size_t)kP2PWMax * 2 * kMailSlot + (size_t)(src * 2 + par) * 4;
+}
+inline size_t mail_ack_off(int dst, int par) {
+  return kP2PRedBytes + (size_t)kP2PWMax * 2 * kMailSlot + 256 + (size_t)(dst * 2 + par) * 4;
+}
+constexpr size_t kP2PBoardBytes = kP2PRedBytes + (size_t)kP2PWMax * 2 * kMailSlot + 512;
 // flag value published for a reduction epoch (0 means "not published")
 inline unsigned p2p_tag(int64_t epoch) { return (unsigned)(epoch & 0x7fffffff) + 1u; }
 

@@ -81,6 +81,7 @@ class LaunchStats:
     transfers: int = 0
     inits: int = 0
     p2p_folds: int = 0  # reductions gathered through the peer-memory boards
+    p2p_halos: int = 0  # transfer sets moved through the peer mailboxes
     mplan_hits: int = 0  # multi-GPU launches replayed from the plan cache
 
 
@@ -126,6 +127,7 @@ class Executor:
         self._comm = False
         self._p2p = False
         self._p2p_epoch = 0
+        self._xepoch: dict[int, int] = {}  # per peer: halo exchanges through the peer mailboxes so far
         # CUDA-graph relaunch of repeated launch segments (enable_graphs)
         self._graphs_on = False
         self._pending: list = []  # deferred plan-cache hits: (handle, views, scalars, nscal, nslots)
@@ -404,10 +406,49 @@ class Executor:
                     his[4 * i + d] = rect[1][d]
                 self.stats.bytes_moved += rg.volume(rect) * r.esize
             self.stats.transfers += n
-            check(self.lib.dk_comm_exchange(n, sids, peers, dirs, los, his))
+            self._exchange(n, sids, peers, dirs, los, his)
             if self._rec is not None:
                 nbytes = sum(rg.volume(t[1]) * self.stores[t[0]].esize for t in mine)
                 self._rec["xfer"] = (n, sids, peers, dirs, los, his, nbytes)
+
+    def _exchange(self, n, sids, peers, dirs, los, his) -> None:
+        """Move the transfer list: pairs whose rects fit a peer mailbox go through peer memory
+        (dk_p2p_exchange), the rest through grouped NCCL send/recv.  The split is per peer pair and
+        computed from the replicated plan, so both ends of a pair decide alike."""
+        use = {}
+        if self._p2p and os.environ.get("DK_P2P_HALO", "1") != "0":
+            per = {}
+            for i in range(n):
+                key = (peers[i], dirs[i])
+                esz = self.stores[sids[i]].esize
+                vol = 1
+                for d in range(len(self.stores[sids[i]].shape)):
+                    vol *= max(0, his[4 * i + d] - los[4 * i + d])
+                b, k = per.get(key, (0, 0))
+                per[key] = (b + ((vol * esz + 15) // 16) * 16, k + 1)
+            for q in {peers[i] for i in range(n)}:
+                fits = all(per.get((q, d), (0, 0))[0] <= runtime.P2P_MAIL_BYTES and per.get((q, d), (0, 0))[1] <= 8
+                           for d in (0, 1))
+                use[q] = fits
+        p2p_idx = [i for i in range(n) if use.get(peers[i])]
+        nccl_idx = [i for i in range(n) if not use.get(peers[i])]
+
+        def sub(idx):
+            m = len(idx)
+            return (m, (c_int64 * m)(*[sids[i] for i in idx]), (c_int32 * m)(*[peers[i] for i in idx]),
+                    (c_int32 * m)(*[dirs[i] for i in idx]),
+                    (c_int64 * (4 * m))(*[los[4 * i + d] for i in idx for d in range(4)]),
+                    (c_int64 * (4 * m))(*[his[4 * i + d] for i in idx for d in range(4)]))
+
+        if p2p_idx:
+            args = sub(p2p_idx) if nccl_idx else (n, sids, peers, dirs, los, his)
+            ep = (c_int64 * self.world)(*[self._xepoch.get(q, 0) for q in range(self.world)])
+            check(self.lib.dk_p2p_exchange(*args, ep))
+            for q in {peers[i] for i in p2p_idx}:
+                self._xepoch[q] = self._xepoch.get(q, 0) + 1
+            self.stats.p2p_halos += 1
+        if nccl_idx:
+            check(self.lib.dk_comm_exchange(*(sub(nccl_idx) if p2p_idx else (n, sids, peers, dirs, los, his))))
 
     def _wrote(self, sid: int, rect, q: int) -> None:
         r = self.stores[sid]
@@ -691,7 +732,7 @@ class Executor:
         x = hit["xfer"]
         if x is not None:
             n, cs, peers, dirs, los, his, nbytes = x
-            check(self.lib.dk_comm_exchange(n, (c_int64 * n)(*[sids[c] for c in cs]), peers, dirs, los, his))
+            self._exchange(n, (c_int64 * n)(*[sids[c] for c in cs]), peers, dirs, los, his)
             self.stats.transfers += n
             self.stats.bytes_moved += nbytes
         if kp is None:

@@ -107,12 +107,18 @@ _SIGS = {
     "dk_p2p_init": (c_int, [POINTER(c_int)]),
     "dk_launch_pub": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_int64, c_int]),
     "dk_p2p_wait": (c_int, [c_int64, POINTER(c_int32), POINTER(c_uint64)]),
+    "dk_p2p_exchange": (
+        c_int,
+        [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64),
+         POINTER(c_int64)],
+    ),
 }
 
 # board geometry of the peer-memory reduction exchange (include/dk_b200.h)
 P2P_SLOTS = 4
 P2P_POINTS = 16
 P2P_RED = 32
+P2P_MAIL_BYTES = 1 << 20
 
 EXPORTED = tuple(_SIGS)
 

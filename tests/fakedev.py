@@ -458,6 +458,29 @@ class FakeLib:
             self._store_array(sid)[sl] = t.numpy().astype(self._store_array(sid).dtype)
         return 0
 
+    def dk_p2p_exchange(self, n, sids, peers, dirs, los, his, epochs):
+        """Peer-mailbox halo moves: same data path as dk_comm_exchange here, plus a check that both
+        ends of every pair use the same exchange epoch (the counters the executor keeps per peer)."""
+        import torch
+        import torch.distributed as dist
+
+        self.p2p_exchanges = getattr(self, "p2p_exchanges", 0) + 1
+        pairs = sorted({peers[i] for i in range(n)})
+        reqs, got = [], {}
+        for q in pairs:
+            mine = torch.tensor([float(epochs[q])], dtype=torch.float64)
+            theirs = torch.empty(1, dtype=torch.float64)
+            lo, hi = (mine, theirs) if self.rank < q else (theirs, mine)
+            reqs.append(dist.isend(mine, q, tag=90000))
+            reqs.append(dist.irecv(theirs, q, tag=90000))
+            got[q] = (mine, theirs)
+        for r in reqs:
+            r.wait()
+        for q, (mine, theirs) in got.items():
+            if float(mine) != float(theirs):
+                raise AssertionError(f"rank {self.rank} and {q} disagree on the exchange epoch: {mine} vs {theirs}")
+        return self.dk_comm_exchange(n, sids, peers, dirs, los, his)
+
     def dk_comm_allgather_f64(self, src, dst, count):
         import torch
         import torch.distributed as dist

@@ -65,7 +65,7 @@ def _worker(rank, world, port, names, q, p2p=False):
         try:
             replay(ex, trace.events)
             got = {s: ex.get(s) for s in trace.live}
-            moved += ex.stats.p2p_folds if p2p else ex.stats.transfers
+            moved += (ex.stats.p2p_folds + ex.stats.p2p_halos) if p2p else ex.stats.transfers
             hits += ex.stats.mplan_hits
             if rank == 0:
                 want = want_arrays if want_arrays is not None else golden_arrays(case)
