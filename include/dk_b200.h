@@ -193,16 +193,17 @@ int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered);
  * (same arguments as dk_comm_exchange).  Each rank's board also holds a
  * mailbox per (source rank, parity) of DK_P2P_MAIL_BYTES: one kernel packs
  * this rank's send rects straight into the receivers' mailboxes over NVLink
- * and raises a flag there (tag of the pair's exchange epoch); its receive CTAs
- * wait for the senders' flags, unpack into the store rects and acknowledge,
- * so a sender reuses a mailbox parity only after the receiver consumed it.
- * `epochs[q]` = number of earlier exchanges between this rank and rank q (the
- * same count on both sides: the plan is replicated).  Fails with
+ * and raises a flag there (tag of the k-th message from this rank to that
+ * peer); its receive CTAs wait for the senders' flags, unpack into the store
+ * rects and acknowledge, so a sender reuses a mailbox parity only after the
+ * receiver consumed the message two before.  The per-direction message
+ * counts live in the library (process lifetime), so every pair of ranks
+ * agrees on them as long as both call this for the pair's moves.  Fails with
  * DK_ERR_UNSUPPORTED if one pair's bytes exceed a mailbox; the caller then
  * uses dk_comm_exchange (the decision is the same on both ranks). */
 #define DK_P2P_MAIL_BYTES (1 << 20)
 int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs, const int64_t* los,
-                    const int64_t* his, const int64_t* epochs);
+                    const int64_t* his);
 
 #ifdef __cplusplus
 }

@@ -159,6 +159,56 @@ __device__ __forceinline__ int64_t x_elem_off(const dk_view& v, int64_t i) {
   return o;
 }
 
+// one CTA moves one rect between a store view and its dense mailbox image:
+// contiguous rects as 16-byte vectors when both ends allow it, else row by row
+// (rank <= 2 views: rows are contiguous runs of ext[rank-1] elements)
+__device__ __forceinline__ void x_copy(const XItem& it, char* dst, const char* src, bool pack) {
+  const int es = it.v.dtype == DK_F64 ? 8 : 4;
+  const int r = it.v.rank;
+  const int64_t inner = r ? it.v.ext[r - 1] : 1;
+  const bool contiguous = r <= 1 || it.v.stride[r - 2] == inner || it.count == inner;
+  if (contiguous) {
+    const int64_t bytes = it.count * es;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+      const int64_t nv = bytes / 16;
+      for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
+        ((int4*)dst)[i] = ((const int4*)src)[i];
+      for (int64_t b = nv * 16 + threadIdx.x * 4; b < bytes; b += blockDim.x * 4)
+        *(int*)(dst + b) = *(const int*)(src + b);
+    } else if (es == 8) {
+      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) ((double*)dst)[i] = ((const double*)src)[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) ((int*)dst)[i] = ((const int*)src)[i];
+    }
+    return;
+  }
+  if (r == 2) {
+    const int64_t rows = it.v.ext[0], rs = it.v.stride[0];
+    for (int64_t row = 0; row < rows; ++row)
+      for (int64_t j = threadIdx.x; j < inner; j += blockDim.x) {
+        const int64_t m = row * inner + j, o = row * rs + j;
+        if (es == 8) {
+          if (pack) ((double*)dst)[m] = ((const double*)src)[o];
+          else ((double*)dst)[o] = ((const double*)src)[m];
+        } else {
+          if (pack) ((int*)dst)[m] = ((const int*)src)[o];
+          else ((int*)dst)[o] = ((const int*)src)[m];
+        }
+      }
+    return;
+  }
+  for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) {
+    const int64_t o = x_elem_off(it.v, i);
+    if (es == 8) {
+      if (pack) ((double*)dst)[i] = ((const double*)src)[o];
+      else ((double*)dst)[o] = ((const double*)src)[i];
+    } else {
+      if (pack) ((int*)dst)[i] = ((const int*)src)[o];
+      else ((int*)dst)[o] = ((const int*)src)[i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_p2p_xchg(XArgs a) {
   const XCta& c = a.cta[blockIdx.x];
   if (c.dir == 0) {
@@ -166,16 +216,7 @@ __global__ void __launch_bounds__(1024) k_p2p_xchg(XArgs a) {
     __syncthreads();
     for (int k = 0; k < c.nitems; ++k) {
       const XItem& it = c.item[k];
-      const int es = it.v.dtype == DK_F64 ? 8 : 4;
-      char* dst = (char*)c.mail + it.off;
-      const char* src = (const char*)it.v.ptr;
-      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) {
-        const int64_t o = x_elem_off(it.v, i);
-        if (es == 8)
-          ((double*)dst)[i] = ((const double*)src)[o];
-        else
-          ((int*)dst)[i] = ((const int*)src)[o];
-      }
+      x_copy(it, (char*)c.mail + it.off, (const char*)it.v.ptr, true);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -187,16 +228,7 @@ __global__ void __launch_bounds__(1024) k_p2p_xchg(XArgs a) {
     __syncthreads();
     for (int k = 0; k < c.nitems; ++k) {
       const XItem& it = c.item[k];
-      const int es = it.v.dtype == DK_F64 ? 8 : 4;
-      const char* src = (const char*)c.mail + it.off;
-      char* dst = (char*)it.v.ptr;
-      for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) {
-        const int64_t o = x_elem_off(it.v, i);
-        if (es == 8)
-          ((double*)dst)[o] = ((const double*)src)[i];
-        else
-          ((int*)dst)[o] = ((const int*)src)[i];
-      }
+      x_copy(it, (char*)it.v.ptr, (const char*)c.mail + it.off, false);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -213,7 +245,7 @@ using namespace dk;
 extern "C" {
 
 int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs, const int64_t* los,
-                    const int64_t* his, const int64_t* epochs) {
+                    const int64_t* his) {
   return guard([&] {
     require_init();
     require_not_capturing("dk_p2p_exchange");
@@ -239,7 +271,7 @@ int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int3
       if (ci < 0) {
         ci = a.ncta++;
         XCta& c = a.cta[ci];
-        const int64_t e = epochs[q];
+        const int64_t e = dir == 0 ? S.xsend[q] : S.xrecv[q];
         const int par = (int)(e & 1);
         c.dir = dir;
         c.tag = p2p_tag(e);
@@ -272,6 +304,10 @@ int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int3
     k_p2p_xchg<<<a.ncta, 1024, 0, S.stream>>>(a);
     DK_CUDA(cudaGetLastError());
     S.launches++;
+    for (int q = 0; q < S.world; ++q) {
+      if (cta_of[0][q] >= 0) S.xsend[q]++;
+      if (cta_of[1][q] >= 0) S.xrecv[q]++;
+    }
   });
 }
 

@@ -120,6 +120,8 @@ struct State {
   bool p2p = false;
   void* board = nullptr;
   uint64_t peer_board[8] = {};
+  // halo mailbox messages sent to / received from each peer so far (dk_p2p_exchange)
+  int64_t xsend[8] = {}, xrecv[8] = {};
 };
 
 // board layout: [slot][kP2PWMax][DK_P2P_POINTS][DK_P2P_RED] doubles, then

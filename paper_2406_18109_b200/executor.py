@@ -127,7 +127,6 @@ class Executor:
         self._comm = False
         self._p2p = False
         self._p2p_epoch = 0
-        self._xepoch: dict[int, int] = {}  # per peer: halo exchanges through the peer mailboxes so far
         # CUDA-graph relaunch of repeated launch segments (enable_graphs)
         self._graphs_on = False
         self._pending: list = []  # deferred plan-cache hits: (handle, views, scalars, nscal, nslots)
@@ -441,11 +440,7 @@ class Executor:
                     (c_int64 * (4 * m))(*[his[4 * i + d] for i in idx for d in range(4)]))
 
         if p2p_idx:
-            args = sub(p2p_idx) if nccl_idx else (n, sids, peers, dirs, los, his)
-            ep = (c_int64 * self.world)(*[self._xepoch.get(q, 0) for q in range(self.world)])
-            check(self.lib.dk_p2p_exchange(*args, ep))
-            for q in {peers[i] for i in p2p_idx}:
-                self._xepoch[q] = self._xepoch.get(q, 0) + 1
+            check(self.lib.dk_p2p_exchange(*(sub(p2p_idx) if nccl_idx else (n, sids, peers, dirs, los, his))))
             self.stats.p2p_halos += 1
         if nccl_idx:
             check(self.lib.dk_comm_exchange(*(sub(nccl_idx) if p2p_idx else (n, sids, peers, dirs, los, his))))

@@ -109,8 +109,7 @@ _SIGS = {
     "dk_p2p_wait": (c_int, [c_int64, POINTER(c_int32), POINTER(c_uint64)]),
     "dk_p2p_exchange": (
         c_int,
-        [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64),
-         POINTER(c_int64)],
+        [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)],
     ),
 }
 

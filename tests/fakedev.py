@@ -458,27 +458,34 @@ class FakeLib:
             self._store_array(sid)[sl] = t.numpy().astype(self._store_array(sid).dtype)
         return 0
 
-    def dk_p2p_exchange(self, n, sids, peers, dirs, los, his, epochs):
-        """Peer-mailbox halo moves: same data path as dk_comm_exchange here, plus a check that both
-        ends of every pair use the same exchange epoch (the counters the executor keeps per peer)."""
+    def dk_p2p_exchange(self, n, sids, peers, dirs, los, his):
+        """Peer-mailbox halo moves: the data path of dk_comm_exchange, plus the library's per-direction
+        message counters -- checked against the peer's (my k-th send to q is q's k-th receive from me)."""
         import torch
         import torch.distributed as dist
 
-        self.p2p_exchanges = getattr(self, "p2p_exchanges", 0) + 1
+        self.xsend = getattr(self, "xsend", {})
+        self.xrecv = getattr(self, "xrecv", {})
         pairs = sorted({peers[i] for i in range(n)})
         reqs, got = [], {}
         for q in pairs:
-            mine = torch.tensor([float(epochs[q])], dtype=torch.float64)
-            theirs = torch.empty(1, dtype=torch.float64)
-            lo, hi = (mine, theirs) if self.rank < q else (theirs, mine)
+            sends = any(peers[i] == q and dirs[i] == 0 for i in range(n))
+            recvs = any(peers[i] == q and dirs[i] == 1 for i in range(n))
+            mine = torch.tensor([float(self.xsend.get(q, 0)) if sends else -1.0,
+                                 float(self.xrecv.get(q, 0)) if recvs else -1.0], dtype=torch.float64)
+            theirs = torch.empty(2, dtype=torch.float64)
             reqs.append(dist.isend(mine, q, tag=90000))
             reqs.append(dist.irecv(theirs, q, tag=90000))
-            got[q] = (mine, theirs)
+            got[q] = (mine, theirs, sends, recvs)
         for r in reqs:
             r.wait()
-        for q, (mine, theirs) in got.items():
-            if float(mine) != float(theirs):
-                raise AssertionError(f"rank {self.rank} and {q} disagree on the exchange epoch: {mine} vs {theirs}")
+        for q, (mine, theirs, sends, recvs) in got.items():
+            if float(mine[0]) != float(theirs[1]) or float(mine[1]) != float(theirs[0]):
+                raise AssertionError(f"rank {self.rank}/{q}: mailbox counters disagree {mine.tolist()} vs {theirs.tolist()}")
+            if sends:
+                self.xsend[q] = self.xsend.get(q, 0) + 1
+            if recvs:
+                self.xrecv[q] = self.xrecv.get(q, 0) + 1
         return self.dk_comm_exchange(n, sids, peers, dirs, los, his)
 
     def dk_comm_allgather_f64(self, src, dst, count):
