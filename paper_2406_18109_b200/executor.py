@@ -415,7 +415,7 @@ class Executor:
         (dk_p2p_exchange), the rest through grouped NCCL send/recv.  The split is per peer pair and
         computed from the replicated plan, so both ends of a pair decide alike."""
         use = {}
-        if self._p2p and os.environ.get("DK_P2P_HALO", "1") != "0":
+        if self._p2p and os.environ.get("DK_P2P_HALO", "0") == "1":
             per = {}
             for i in range(n):
                 key = (peers[i], dirs[i])
