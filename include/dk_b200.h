@@ -204,6 +204,18 @@ int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered);
 #define DK_P2P_MAIL_BYTES (1 << 20)
 int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int32_t* dirs, const int64_t* los,
                     const int64_t* his);
+/* The same mailbox protocol driven by copy engines and stream memory operations
+ * (no SMs), so a halo can move while a persistent kernel owns the SMs:
+ * dk_dma_send -- on the current stream: per peer, wait (cuStreamWaitValue32)
+ * for the receiver's ack of the message two before, copy the (contiguous)
+ * rects into its mailbox over NVLink (cudaMemcpyAsync), then write the
+ * message tag into its mail flag (cuStreamWriteValue32, fenced);
+ * dk_dma_recv -- on the current stream: per peer, wait for the tag, copy the
+ * mailbox into the store rects, write the ack into the sender's board.
+ * dirs are implied (all sends / all receives); counters shared with
+ * dk_p2p_exchange. */
+int dk_dma_send(int n, const int64_t* sids, const int32_t* peers, const int64_t* los, const int64_t* his);
+int dk_dma_recv(int n, const int64_t* sids, const int32_t* peers, const int64_t* los, const int64_t* his);
 
 #ifdef __cplusplus
 }

@@ -106,8 +106,9 @@ __global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world, uns
 // publishes the epoch's tag into the receiver's mail flag with release
 // semantics at system scope.  A receive CTA waits for that tag (acquire),
 // copies the mailbox into its store rects and acks into the sender's board.
-// A flag or ack holding an unexpected nonzero tag traps; 10 s without
-// progress traps (never a hang).
+// Flags and acks hold the tag of the latest message (never cleared: the
+// next value a parity sees is two messages on); 10 s without progress traps
+// (never a hang).
 constexpr int kXMaxItems = 8;
 struct XItem {
   dk_view v;     // store rect (8- or 4-byte elements)
@@ -135,11 +136,7 @@ __device__ __forceinline__ void x_wait(const unsigned int* f, unsigned tag, cons
   for (;;) {
     unsigned int v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (v == tag) return;
-    if (v != 0u && what[0] == 'm') {  // a mail flag from another epoch
-      printf("dk_p2p_exchange: cta %d mail flag holds tag %u, expected %u\n", cta, v, tag);
-      __trap();
-    }
+    if (v == tag) return;  // flags hold the latest message's tag (never cleared)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > 10000000000ull) {
       printf("dk_p2p_exchange: cta %d timed out waiting for %s tag %u (last %u)\n", cta, what, tag, v);
@@ -231,10 +228,8 @@ __global__ void __launch_bounds__(1024) k_p2p_xchg(XArgs a) {
       x_copy(it, (char*)it.v.ptr, (const char*)c.mail + it.off, false);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      *(volatile unsigned int*)c.flag = 0u;  // consumed (the sender's next write here is two epochs on)
+    if (threadIdx.x == 0)
       asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(c.ack), "r"(c.tag) : "memory");
-    }
   }
 }
 
@@ -308,6 +303,75 @@ int dk_p2p_exchange(int n, const int64_t* sids, const int32_t* peers, const int3
       if (cta_of[0][q] >= 0) S.xsend[q]++;
       if (cta_of[1][q] >= 0) S.xrecv[q]++;
     }
+  });
+}
+
+static void dma_move(int n, const int64_t* sids, const int32_t* peers, const int64_t* los, const int64_t* his,
+                     bool send) {
+  require_init();
+  require_not_capturing(send ? "dk_dma_send" : "dk_dma_recv");
+  State& S = st();
+  if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer memory");
+  CUstream cs = (CUstream)S.stream;
+  // group the rects by peer, in order (both ends see the same order: the plan is replicated)
+  for (int q = 0; q < S.world; ++q) {
+    int64_t off = 0;
+    bool any = false;
+    const int64_t k = send ? S.xsend[q] : S.xrecv[q];
+    const int par = (int)(k & 1);
+    const unsigned tag = p2p_tag(k);
+    for (int i = 0; i < n; ++i) {
+      if (peers[i] != q) continue;
+      if (q == S.rank || q < 0 || q >= S.world) fail(DK_ERR_ARG, "bad peer %d", q);
+      Store& so = store_of(sids[i]);
+      RectView rv = rect_view(so, los + 4 * i, his + 4 * i);
+      if (rv.count == 0) continue;
+      if (!rv.contiguous) fail(DK_ERR_UNSUPPORTED, "dk_dma_*: rect of store %lld is not contiguous", (long long)sids[i]);
+      store_ensure_bytes(so, (size_t)rv.first * so.esize, (size_t)(rv.first + rv.count) * so.esize);
+      const size_t bytes = (size_t)rv.count * so.esize;
+      if (off + (int64_t)bytes > (int64_t)kMailSlot) fail(DK_ERR_UNSUPPORTED, "halo exceeds the mailbox");
+      void* store_ptr = (void*)((uint64_t)so.base + (uint64_t)rv.first * so.esize);
+      if (!any) {
+        any = true;
+        if (send && k >= 2)  // the receiver consumed the message two before on this parity
+          DK_CU(cuStreamWaitValue32(cs, (CUdeviceptr)((uint64_t)S.board + mail_ack_off(q, par)), p2p_tag(k - 2),
+                                    CU_STREAM_WAIT_VALUE_GEQ));
+        if (!send)
+          DK_CU(cuStreamWaitValue32(cs, (CUdeviceptr)((uint64_t)S.board + mail_flag_off(q, par)), tag,
+                                    CU_STREAM_WAIT_VALUE_EQ));
+      }
+      if (send)
+        DK_CUDA(cudaMemcpyAsync((void*)(S.peer_board[q] + mail_data_off(S.rank, par) + off), store_ptr, bytes,
+                                cudaMemcpyDeviceToDevice, S.stream));
+      else
+        DK_CUDA(cudaMemcpyAsync(store_ptr, (void*)((uint64_t)S.board + mail_data_off(q, par) + off), bytes,
+                                cudaMemcpyDeviceToDevice, S.stream));
+      off += (int64_t)((bytes + 15) & ~(size_t)15);
+    }
+    if (!any) continue;
+    if (send) {
+      DK_CU(cuStreamWriteValue32(cs, (CUdeviceptr)(S.peer_board[q] + mail_flag_off(S.rank, par)), tag,
+                                 CU_STREAM_WRITE_VALUE_DEFAULT));
+      S.xsend[q]++;
+    } else {
+      DK_CU(cuStreamWriteValue32(cs, (CUdeviceptr)(S.peer_board[q] + mail_ack_off(S.rank, par)), tag,
+                                 CU_STREAM_WRITE_VALUE_DEFAULT));
+      S.xrecv[q]++;
+    }
+  }
+}
+
+int dk_dma_send(int n, const int64_t* sids, const int32_t* peers, const int64_t* los, const int64_t* his) {
+  return guard([&] {
+    NvtxRange nv("dk_dma_send", n);
+    dma_move(n, sids, peers, los, his, true);
+  });
+}
+
+int dk_dma_recv(int n, const int64_t* sids, const int32_t* peers, const int64_t* los, const int64_t* his) {
+  return guard([&] {
+    NvtxRange nv("dk_dma_recv", n);
+    dma_move(n, sids, peers, los, his, false);
   });
 }
 

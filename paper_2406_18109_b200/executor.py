@@ -127,6 +127,8 @@ class Executor:
         self._comm = False
         self._p2p = False
         self._p2p_epoch = 0
+        self._side = None  # side stream (+ events) of the overlapped SpMV halo sends
+        self._side_ev = None
         # CUDA-graph relaunch of repeated launch segments (enable_graphs)
         self._graphs_on = False
         self._pending: list = []  # deferred plan-cache hits: (handle, views, scalars, nscal, nslots)
@@ -348,8 +350,11 @@ class Executor:
             return ordinal * self.world // volume
         return ordinal
 
-    def _satisfy(self, need: dict[int, dict[int, list]]) -> None:
-        """Make every rank's needed rects valid (same plan on every rank)."""
+    def _satisfy(self, need: dict[int, dict[int, list]], defer: bool = False):
+        """Make every rank's needed rects valid (same plan on every rank).
+
+        ``defer``: plan (and book) the transfers but return this rank's share,
+        ``[(sid, rect, src, dst)]``, for the caller to move; initialisations run now."""
         snap = {sid: [list(v) for v in self.stores[sid].valid] for sid in {s for d in need.values() for s in d}}
         transfers = []  # (sid, rect, src, dst)
         inits: dict[int, list] = {}
@@ -384,6 +389,12 @@ class Executor:
         for sid, rects in inits.items():
             self._materialize_init(self.stores[sid], rects)
         mine = [t for t in transfers if self.rank in (t[2], t[3])]
+        if defer:
+            for sid, rect, _src, _dst in mine:
+                self._ensure(self.stores[sid], rect)
+                self.stats.bytes_moved += rg.volume(rect) * self.stores[sid].esize
+            self.stats.transfers += len(mine)
+            return mine
         if mine:
             if not self._comm:
                 raise BackendError("multi-rank transfer without an initialised communicator")
@@ -841,10 +852,23 @@ class Executor:
                         need.setdefault(q, {}).setdefault(a.store, []).append(rect)
         if multi:
             self._check_cross_rank(task, prank, rects, reads, writes, temp_positions)
-        self._satisfy(need)
+        overlap = kp is None and self._spmv_overlap_ok(task, prank)
+        if overlap:
+            # the x halo moves by copy engine while the interior rows run (_run_spmv_overlap)
+            lay, own, halo_need = self._spmv_split(task, pts)
+            for q in range(self.world):
+                need[q][task.args[3].store] = [own[q]]
+            self._satisfy(need)
+            moves = self._satisfy(halo_need, defer=True)
+        else:
+            self._satisfy(need)
 
         mine = [i for i in range(V) if prank[i] == self.rank]
-        if kp is None:
+        if overlap:
+            if self._rec is not None:
+                self._rec["ok"] = False
+            self._run_spmv_overlap(task, pts, mine, rects, lay, moves)
+        elif kp is None:
             self._run_builtin(task, pts, mine, rects, prank)
         else:
             recorded = self._run_kernel(task, kp, mine, prank, rects, temp_positions, reduces, isolated, spmv_dot)
@@ -875,6 +899,100 @@ class Executor:
                     for o in range(self.world):
                         r.valid[o] = rg.add(r.valid[o], r.full)
                     r.written = rg.add(r.written, r.full)
+
+    # ------------------------------------------- SpMV with an overlapped halo
+    # One tile per rank of the row-band Poisson matrix: rows [nx, t - nx) of a
+    # tile reference only x rows the rank owns, so they run while the two
+    # one-grid-row halos come in by copy engine (dk_dma_send on a side stream,
+    # dk_dma_recv on the main stream after the interior rows); the boundary
+    # rows follow.  Same kernels, same per-row order: bit-identical results.
+    def _spmv_overlap_ok(self, task: TaskDesc, prank) -> bool:
+        if not (self.world > 1 and self._p2p and task.kind == "SPMV_CSR"
+                and os.environ.get("DK_OVERLAP_HALO", "1") == "1"):
+            return False
+        spec = self.init.get(task.args[1].store)
+        if not spec or spec.get("kind") != "csr_cols" or int(spec["k"]) != len(prank):
+            return False
+        if list(prank) != list(range(self.world)) or task.launch != (self.world,):
+            return False
+        lay = poisson_tile_layout(int(spec["nx"]), int(spec["ny"]), int(spec["k"]))
+        return lay["t"] > 2 * lay["nx"] and self.shape(task.args[3].store) == (lay["n"],) \
+            and task.args[3].part.is_none
+
+    def _spmv_split(self, task: TaskDesc, pts):
+        spec = self.init[task.args[1].store]
+        lay = poisson_tile_layout(int(spec["nx"]), int(spec["ny"]), int(spec["k"]))
+        t, n = lay["t"], lay["n"]
+        xs = task.args[3].store
+        own = {q: ((q * t,), ((q + 1) * t,)) for q in range(self.world)}
+        halo = {}
+        for q in range(self.world):
+            f = self._csr_footprint(task, pts[q], ((0,), (n,)))
+            parts = [x for x in rg.minus([f], [own[q]]) if not rg.empty(x)]
+            halo[q] = {xs: parts}
+        return lay, own, halo
+
+    def _run_spmv_overlap(self, task, pts, mine, rects, lay, moves) -> None:
+        t, nx = lay["t"], lay["nx"]
+        i = mine[0]
+        r_rp, r_cl, r_vl, r_x, r_y = (self.stores[a.store] for a in task.args)
+        for rec, rect in zip((r_rp, r_cl, r_vl, r_x, r_y), rects[i]):
+            self._ensure(rec, rect)
+
+        def enc(lst):
+            m = len(lst)
+            sids = (c_int64 * max(m, 1))(*[x[0] for x in lst])
+            peers = (c_int32 * max(m, 1))(*[(x[3] if x[2] == self.rank else x[2]) for x in lst])
+            los = (c_int64 * (4 * max(m, 1)))()
+            his = (c_int64 * (4 * max(m, 1)))()
+            for k, x in enumerate(lst):
+                los[4 * k], his[4 * k] = x[1][0][0], x[1][1][0]
+            return m, sids, peers, los, his
+
+        sends = [x for x in moves if x[2] == self.rank]
+        recvs = [x for x in moves if x[3] == self.rank]
+        main = self.stream()
+        if self._side is None:
+            s = c_uint64()
+            check(self.lib.dk_stream_new(byref(s)))
+            self._side = s.value
+            evs = []
+            for _ in range(2):
+                e = c_uint64()
+                check(self.lib.dk_event_new(byref(e)))
+                evs.append(e.value)
+            self._side_ev = evs
+        if sends:
+            check(self.lib.dk_event_record(self._side_ev[0]))  # p is final on the main stream here
+            check(self.lib.dk_set_stream(self._side))
+            try:
+                check(self.lib.dk_stream_wait_event(self._side_ev[0]))
+                check(self.lib.dk_dma_send(*enc(sends)))
+                check(self.lib.dk_event_record(self._side_ev[1]))
+            finally:
+                check(self.lib.dk_set_stream(main))
+        rp0, y0 = rects[i][0][0][0], rects[i][4][0][0]
+        wflags = (c_int32 * 5)(0, 0, 0, 0, 1)
+
+        def rows(a, b):
+            if b <= a:
+                return
+            views = (dk_view * 5)()
+            views[0] = self.view(r_rp, ((rp0 + a,), (rp0 + b + 1,)))
+            views[1] = self.view(r_cl, rects[i][1])
+            views[2] = self.view(r_vl, rects[i][2])
+            views[3] = self.view(r_x, r_x.full)
+            views[4] = self.view(r_y, ((y0 + a,), (y0 + b,)))
+            check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
+
+        rows(nx, t - nx)  # interior: only this rank's own x rows
+        if recvs:
+            check(self.lib.dk_dma_recv(*enc(recvs)))
+        rows(0, nx)
+        rows(t - nx, t)
+        if sends:
+            check(self.lib.dk_stream_wait_event(self._side_ev[1]))  # p is not rewritten before the sends read it
+        self.stats.p2p_halos += 1
 
     def _csr_footprint(self, task: TaskDesc, p, full):
         """Columns of x an SPMV_CSR tile actually reads (NonePart reads the whole store).

@@ -488,6 +488,65 @@ class FakeLib:
                 self.xrecv[q] = self.xrecv.get(q, 0) + 1
         return self.dk_comm_exchange(n, sids, peers, dirs, los, his)
 
+    # streams / events: the stand-in executes every call at once, in call order
+    def dk_stream_new(self, ref):
+        _set(ref, 1000 + getattr(self, "_nstreams", 0))
+        self._nstreams = getattr(self, "_nstreams", 0) + 1
+        return 0
+
+    def dk_event_new(self, ref):
+        _set(ref, 2000 + getattr(self, "_nevents", 0))
+        self._nevents = getattr(self, "_nevents", 0) + 1
+        return 0
+
+    def dk_event_record(self, e):
+        return 0
+
+    def dk_stream_wait_event(self, e):
+        return 0
+
+    def dk_dma_send(self, n, sids, peers, los, his):
+        """Copy-engine halo sends: posted now (isend), completed by the matching dk_dma_recv."""
+        import torch
+        import torch.distributed as dist
+
+        self.xsend = getattr(self, "xsend", {})
+        self._dma_pending = getattr(self, "_dma_pending", [])
+        for q in sorted({peers[i] for i in range(n)}):
+            items = [i for i in range(n) if peers[i] == q]
+            data = [np.ascontiguousarray(self._store_array(sids[i])[los[4 * i]:his[4 * i]]).astype(np.float64)
+                    for i in items]
+            msg = np.concatenate([[float(self.xsend.get(q, 0))]] + data)
+            t = torch.from_numpy(msg.copy())
+            self._dma_pending.append(dist.isend(t, q, tag=91000))
+            self._dma_keep = getattr(self, "_dma_keep", []) + [t]
+            self.xsend[q] = self.xsend.get(q, 0) + 1
+        return 0
+
+    def dk_dma_recv(self, n, sids, peers, los, his):
+        import torch
+        import torch.distributed as dist
+
+        self.xrecv = getattr(self, "xrecv", {})
+        for q in sorted({peers[i] for i in range(n)}):
+            items = [i for i in range(n) if peers[i] == q]
+            sizes = [his[4 * i] - los[4 * i] for i in items]
+            t = torch.empty(1 + sum(sizes), dtype=torch.float64)
+            dist.recv(t, q, tag=91000)
+            msg = t.numpy()
+            if int(msg[0]) != self.xrecv.get(q, 0):
+                raise AssertionError(f"rank {self.rank}: message {int(msg[0])} from {q}, expected {self.xrecv.get(q, 0)}")
+            off = 1
+            for i, sz in zip(items, sizes):
+                self._store_array(sids[i])[los[4 * i]:his[4 * i]] = msg[off:off + sz]
+                off += sz
+            self.xrecv[q] = self.xrecv.get(q, 0) + 1
+        for h in getattr(self, "_dma_pending", []):
+            h.wait()
+        self._dma_pending = []
+        self._dma_keep = []
+        return 0
+
     def dk_comm_allgather_f64(self, src, dst, count):
         import torch
         import torch.distributed as dist

@@ -73,6 +73,9 @@ def multirank():
         ("stencil_bands_n4_k8", lambda it: W.stencil_bands(4, 8, it), 3),
         ("cg_csr_8x16_k8", lambda it: W.cg_csr(8, 16, 8, it), 4),
         ("pcg_csr_8x16_k8", lambda it: W.pcg_csr(8, 16, 8, it), 4),
+        # one tile per rank at world 4 with interior rows (t = 64 > 2 nx): the overlapped-halo SpMV
+        ("cg_csr_4x64_k4", lambda it: W.cg_csr(4, 64, 4, it), 4),
+        ("pcg_csr_4x64_k4", lambda it: W.pcg_csr(4, 64, 4, it), 4),
     ]:
         for fused in (True, False):
             tr = capture(f"{name}/{'fused' if fused else 'unfused'}", gen, iters, fused)
