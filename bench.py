@@ -504,6 +504,9 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
     end = torch.cuda.Event(enable_timing=True)
     start.record(ext_stream)
     th0 = time.perf_counter()
+    trace_ts = os.environ.get("DK_TRACE_TS") == "1"
+    if trace_ts:
+        ex.trace_timestamps()
     for i in timed:
         if cycled:
             fresh_targets(ex, trace, its[i])  # host-side frees of 8-byte stores (only when cycling)
@@ -512,7 +515,9 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
                 if with_events:
                     a = torch.cuda.Event(enable_timing=True)
                     a.record(ext_stream)
+                ex.mark(f"start {e.task.kind}/{e.f}")
                 ex.execute(e.task, e.kernel, e.temp_positions)
+                ex.mark(f"end {e.task.kind}/{e.f}")
                 if with_events:
                     b = torch.cuda.Event(enable_timing=True)
                     b.record(ext_stream)
@@ -550,6 +555,8 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
             mine = [i for i in range(e.task.volume) if ex.point_rank(i, e.task.volume) == rank]
             it_bytes += launch_bytes(e.task, e.kernel, e.temp_positions, trace.shapes, trace.dtypes, mine, trace.init)
     measure.next_iteration = steady + ((warmup + steps) % (len(its) - steady))
+    measure.timestamps = ex.timestamps() if trace_ts else None
+    ex._ts = None
     return ms, launches, dom, it_bytes
 
 
@@ -842,6 +849,18 @@ def run_ours(args):
             per_rank = gather_all(torch, world, ms / (steps or args.steps))
             host_rank = gather_all(torch, world, measure.host_ms / (steps or args.steps))
             ms = reduce_max(torch, world, ms)
+            if measure.timestamps:
+                # per-rank device timelines (globaltimer ns), for the multi-GPU step analysis
+                import torch.distributed as dist
+
+                allts = [None] * world
+                if world > 1:
+                    dist.all_gather_object(allts, measure.timestamps)
+                else:
+                    allts = [measure.timestamps]
+                if rank == 0:
+                    with open(os.environ.get("DK_TRACE_OUT", f"ts_{wl}_n{world}.json"), "w") as fh:
+                        json.dump(allts, fh)
             per_exec_ranks = None
             if world > 1 and dom is not None:
                 import torch.distributed as dist

@@ -173,6 +173,9 @@ int dk_comm_barrier(void);
 #define DK_P2P_SLOTS 4
 #define DK_P2P_POINTS 16
 #define DK_P2P_RED 32
+/* diagnostics: a one-thread kernel writes %globaltimer (ns) to ((uint64_t*)buf)[idx] when the
+ * stream reaches it -- per-rank device timelines of the multi-GPU step (bench DK_TRACE_TS) */
+int dk_timestamp(uint64_t buf, int64_t idx);
 /* collective (after dk_comm_init): *enabled = 1 iff every rank mapped every peer's board */
 int dk_p2p_init(int* enabled);
 /* dk_launch with totals published to all ranks' boards for reduction number

@@ -161,6 +161,7 @@ void launch_accum(const dk_view& target, const double* vals, int64_t stride, int
 void launch_builtin(const std::string& kind, const dk_view* v, int n, const int32_t* writes, cudaStream_t s);
 int launch_spmv_csr_dot(const dk_view* v, double* parts, int64_t x_row0, cudaStream_t s);
 void launch_fill(double* p, int64_t n, double value, cudaStream_t s);
+void launch_timestamp(uint64_t buf, int64_t idx, cudaStream_t s);
 void launch_pack(const dk_view& src, double* dst, cudaStream_t s, bool unpack);
 
 inline int64_t view_volume(const dk_view& v) {

@@ -54,6 +54,17 @@ __global__ void k_fill(double* p, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
+__global__ void k_timestamp(unsigned long long* buf, int64_t idx) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  buf[idx] = t;
+}
+
+void launch_timestamp(uint64_t buf, int64_t idx, cudaStream_t s) {
+  k_timestamp<<<1, 1, 0, s>>>((unsigned long long*)buf, idx);
+  DK_CUDA(cudaGetLastError());
+}
+
 void launch_fill(double* p, int64_t n, double value, cudaStream_t s) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)st().sm_count * 8);
   k_fill<<<blocks, 256, 0, s>>>(p, n, value);

@@ -202,6 +202,13 @@ int dk_device_info(int* sm_count, int64_t* free_bytes, int64_t* total_bytes) {
   });
 }
 
+int dk_timestamp(uint64_t buf, int64_t idx) {
+  return guard([&] {
+    require_init();
+    launch_timestamp(buf, idx, st().stream);
+  });
+}
+
 int dk_launch_count(int64_t* count) {
   return guard([&] { *count = st().launches; });
 }

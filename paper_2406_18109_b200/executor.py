@@ -127,6 +127,7 @@ class Executor:
         self._comm = False
         self._p2p = False
         self._p2p_epoch = 0
+        self._ts = None  # diagnostics: (device buffer, capacity, [labels]) for mark()
         self._side = None  # side stream (+ events) of the overlapped SpMV halo sends
         self._side_ev = None
         # CUDA-graph relaunch of repeated launch segments (enable_graphs)
@@ -581,6 +582,31 @@ class Executor:
             return
         self._execute_planned(task, kp, temp_positions, pkey)
 
+    # ------------------------------------------------ diagnostics
+    def trace_timestamps(self, capacity: int = 1 << 16) -> None:
+        """Start recording device timestamps at mark() points (bench DK_TRACE_TS)."""
+        p = c_uint64()
+        check(self.lib.dk_scratch_alloc(8 * capacity, byref(p)))
+        self._ts = (p.value, capacity, [])
+
+    def mark(self, label: str) -> None:
+        if self._ts is None:
+            return
+        buf, cap, labels = self._ts
+        if len(labels) < cap:
+            check(self.lib.dk_timestamp(buf, len(labels)))
+            labels.append(label)
+
+    def timestamps(self):
+        """[(label, globaltimer ns)] recorded so far (synchronises)."""
+        if self._ts is None:
+            return []
+        buf, cap, labels = self._ts
+        self.sync()
+        out = np.empty(max(len(labels), 1), dtype=np.uint64)
+        check(self.lib.dk_memcpy_d2h(out.ctypes.data, buf, 8 * len(labels)))
+        return list(zip(labels, out[: len(labels)].tolist()))
+
     # ------------------------------------------------ graph relaunch (f3)
     # With graphs enabled (GpuSession, one GPU), launches that hit the launch-plan
     # cache are not issued at once but collected into a segment; the segment ends
@@ -755,7 +781,9 @@ class Executor:
                 for sir, cv in enumerate(hit["views"]):
                     check(self.lib.dk_launch_pub(h, self._rebind(cv, bases), nsl, scal, ns, epoch, sir))
                 g = c_uint64()
+                self.mark("pub_done")
                 check(self.lib.dk_p2p_wait(epoch, hit["counts"], byref(g)))
+                self.mark("wait_done")
                 for cv, first, stride, nv in hit["fold"]:
                     check(self.lib.dk_accum(byref(self._rebind(cv, bases)), g.value, first, stride, nv))
                 self.stats.p2p_folds += 1
@@ -986,8 +1014,10 @@ class Executor:
             check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
 
         rows(nx, t - nx)  # interior: only this rank's own x rows
+        self.mark("interior_done")
         if recvs:
             check(self.lib.dk_dma_recv(*enc(recvs)))
+        self.mark("halo_in")
         rows(0, nx)
         rows(t - nx, t)
         if sends:
@@ -1270,7 +1300,9 @@ class Executor:
             check(self.lib.dk_scratch_free(totals))
         elif pub_slot >= 0:
             g = c_uint64()
+            self.mark("pub_done")
             check(self.lib.dk_p2p_wait(pub_slot, (c_int32 * self.world)(*counts), byref(g)))
+            self.mark("wait_done")
             self._fold(task, kp, prank, rects, red_targets, g.value, runtime.P2P_POINTS, nred)
             self.stats.p2p_folds += 1
         return recorded

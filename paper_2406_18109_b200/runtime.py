@@ -105,6 +105,7 @@ _SIGS = {
     "dk_comm_allgather_f64": (c_int, [c_uint64, c_uint64, c_int64]),
     "dk_comm_barrier": (c_int, []),
     "dk_p2p_init": (c_int, [POINTER(c_int)]),
+    "dk_timestamp": (c_int, [c_uint64, c_int64]),
     "dk_launch_pub": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_int64, c_int]),
     "dk_p2p_wait": (c_int, [c_int64, POINTER(c_int32), POINTER(c_uint64)]),
     "dk_dma_send": (c_int, [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
