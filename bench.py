@@ -491,14 +491,15 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
             fresh_targets(ex, trace, its[i])
         replay(ex, its[i])
     ex.sync()
+    # no cyclic-GC pauses inside the timed region (earlier workloads' traces
+    # leave millions of objects for a full collection to walk); collected before
+    # the barrier, so no rank starts its timed region a collection late
+    gc.collect()
+    gc.disable()
     if sync_ranks is not None:
         sync_ranks()  # every rank starts its timed region together (warm-up lengths differ)
     timed = seq[steady + warmup:]
     ev = []
-    # no cyclic-GC pauses inside the timed region (earlier workloads' traces
-    # leave millions of objects for a full collection to walk)
-    gc.collect()
-    gc.disable()
     n0 = ex.launch_count()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
