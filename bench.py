@@ -494,6 +494,10 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
     # no cyclic-GC pauses inside the timed region (earlier workloads' traces
     # leave millions of objects for a full collection to walk); collected before
     # the barrier, so no rank starts its timed region a collection late
+    trace_ts = os.environ.get("DK_TRACE_TS") == "1"
+    if trace_ts:
+        ex.trace_timestamps()
+        ex.sync()
     gc.collect()
     gc.disable()
     if sync_ranks is not None:
@@ -505,9 +509,6 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
     end = torch.cuda.Event(enable_timing=True)
     start.record(ext_stream)
     th0 = time.perf_counter()
-    trace_ts = os.environ.get("DK_TRACE_TS") == "1"
-    if trace_ts:
-        ex.trace_timestamps()
     for i in timed:
         if cycled:
             fresh_targets(ex, trace, its[i])  # host-side frees of 8-byte stores (only when cycling)

@@ -191,6 +191,14 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
  * other epoch's tag is a protocol violation and traps; *gathered = the slot's
  * totals, layout [world][DK_P2P_POINTS][nred] as dk_accum's `vals` */
 int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered);
+/* dk_p2p_wait and the point-order fold in one kernel: after the flags, the
+ * kernel applies, in order, target[f] = target[f] + g[first[f] + k*stride[f]]
+ * for k < n[f] (g = the slot's gathered totals) to nfold (<= DK_P2P_FOLDS)
+ * scalar targets (device pointers to fp64) -- what dk_accum would do per fold,
+ * without the extra launches on the reduction's critical path. */
+#define DK_P2P_FOLDS 64
+int dk_p2p_wait_fold(int64_t epoch, const int32_t* counts, int nfold, const uint64_t* targets,
+                     const int64_t* firsts, const int64_t* strides, const int32_t* ns);
 
 /* Halo / replicated-read moves over peer memory instead of NCCL send/recv
  * (same arguments as dk_comm_exchange).  Each rank's board also holds a

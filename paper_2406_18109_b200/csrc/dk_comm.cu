@@ -75,6 +75,50 @@ struct P2PCounts {
   int c[kP2PWMax];
 };
 
+struct P2PFolds {
+  int n;
+  uint64_t target[DK_P2P_FOLDS];
+  int64_t first[DK_P2P_FOLDS], stride[DK_P2P_FOLDS];
+  int32_t cnt[DK_P2P_FOLDS];
+};
+
+__global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world, unsigned tag);
+
+// wait for the slot's flags, then fold in the given order (one thread: the
+// order of the adds is the reference's point order, executor.py:193-195)
+__global__ void k_p2p_wait_fold(unsigned int* flags, P2PCounts counts, int world, unsigned tag, const double* g,
+                                P2PFolds f) {
+  const int q = threadIdx.x / DK_P2P_POINTS, j = threadIdx.x % DK_P2P_POINTS;
+  if (q < world && j < counts.c[q]) {
+    unsigned int* fl = flags + q * DK_P2P_POINTS + j;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+      if (v == tag) break;
+      if (v != 0u) {
+        printf("dk_p2p_wait_fold: rank %d point %d flag holds tag %u, expected %u\n", q, j, v, tag);
+        __trap();
+      }
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) __trap();
+      __nanosleep(64);
+    }
+    *fl = 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < f.n; ++i) {
+      double* tp = (double*)f.target[i];
+      double a = *tp;
+      for (int k = 0; k < f.cnt[i]; ++k) a = __dadd_rn(a, g[f.first[i] + k * f.stride[i]]);
+      *tp = a;
+    }
+  }
+}
+
 __global__ void k_p2p_wait(unsigned int* flags, P2PCounts counts, int world, unsigned tag) {
   const int q = threadIdx.x / DK_P2P_POINTS, j = threadIdx.x % DK_P2P_POINTS;
   if (q < world && j < counts.c[q]) {
@@ -556,6 +600,39 @@ int dk_p2p_wait(int64_t epoch, const int32_t* counts, uint64_t* gathered) {
     DK_CUDA(cudaGetLastError());
     S.launches++;
     *gathered = (uint64_t)(b + p2p_data_off(slot));
+  });
+}
+
+int dk_p2p_wait_fold(int64_t epoch, const int32_t* counts, int nfold, const uint64_t* targets,
+                     const int64_t* firsts, const int64_t* strides, const int32_t* ns) {
+  return guard([&] {
+    require_init();
+    require_not_capturing("dk_p2p_wait_fold");
+    NvtxRange nv("dk_p2p_wait_fold", epoch);
+    State& S = st();
+    if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
+    if (epoch < 0) fail(DK_ERR_ARG, "negative reduction epoch");
+    if (nfold < 0 || nfold > DK_P2P_FOLDS) fail(DK_ERR_ARG, "%d folds (max %d)", nfold, DK_P2P_FOLDS);
+    const int slot = (int)(epoch % DK_P2P_SLOTS);
+    P2PCounts pc = {};
+    for (int q = 0; q < S.world; ++q) {
+      if (counts[q] < 0 || counts[q] > DK_P2P_POINTS) fail(DK_ERR_ARG, "rank %d publishes %d points", q, counts[q]);
+      pc.c[q] = counts[q];
+    }
+    P2PFolds f = {};
+    f.n = nfold;
+    for (int i = 0; i < nfold; ++i) {
+      f.target[i] = targets[i];
+      f.first[i] = firsts[i];
+      f.stride[i] = strides[i];
+      f.cnt[i] = ns[i];
+    }
+    char* b = (char*)S.board;
+    k_p2p_wait_fold<<<1, kP2PWMax * DK_P2P_POINTS, 0, S.stream>>>((unsigned int*)(b + p2p_flag_off(slot)), pc,
+                                                                 S.world, p2p_tag(epoch),
+                                                                 (const double*)(b + p2p_data_off(slot)), f);
+    DK_CUDA(cudaGetLastError());
+    S.launches++;
   });
 }
 

@@ -128,6 +128,7 @@ class Executor:
         self._p2p = False
         self._p2p_epoch = 0
         self._ts = None  # diagnostics: (device buffer, capacity, [labels]) for mark()
+        self._collect = None  # fold ops being gathered for dk_p2p_wait_fold
         self._side = None  # side stream (+ events) of the overlapped SpMV halo sends
         self._side_ev = None
         # CUDA-graph relaunch of repeated launch segments (enable_graphs)
@@ -780,12 +781,10 @@ class Executor:
                 self._p2p_epoch += 1
                 for sir, cv in enumerate(hit["views"]):
                     check(self.lib.dk_launch_pub(h, self._rebind(cv, bases), nsl, scal, ns, epoch, sir))
-                g = c_uint64()
                 self.mark("pub_done")
-                check(self.lib.dk_p2p_wait(epoch, hit["counts"], byref(g)))
+                self._p2p_fold(epoch, hit["counts"], [(self._rebind(cv, bases), first, stride, nv)
+                                                      for cv, first, stride, nv in hit["fold"]])
                 self.mark("wait_done")
-                for cv, first, stride, nv in hit["fold"]:
-                    check(self.lib.dk_accum(byref(self._rebind(cv, bases)), g.value, first, stride, nv))
                 self.stats.p2p_folds += 1
             else:
                 for cv in hit["views"]:
@@ -1299,18 +1298,40 @@ class Executor:
                 self._fold(task, kp, prank, rects, red_targets, gathered, maxp, nred)
             check(self.lib.dk_scratch_free(totals))
         elif pub_slot >= 0:
-            g = c_uint64()
             self.mark("pub_done")
-            check(self.lib.dk_p2p_wait(pub_slot, (c_int32 * self.world)(*counts), byref(g)))
+            ops = []
+            self._collect = ops
+            try:
+                self._fold(task, kp, prank, rects, red_targets, 0, runtime.P2P_POINTS, nred)
+            finally:
+                self._collect = None
+            self._p2p_fold(pub_slot, (c_int32 * self.world)(*counts), ops)
             self.mark("wait_done")
-            self._fold(task, kp, prank, rects, red_targets, g.value, runtime.P2P_POINTS, nred)
             self.stats.p2p_folds += 1
         return recorded
 
     def _accum(self, sid, tv, gathered, first, stride, n) -> None:
-        check(self.lib.dk_accum(byref(tv), gathered, first, stride, n))
+        if self._collect is not None:
+            self._collect.append((tv, first, stride, n))
+        else:
+            check(self.lib.dk_accum(byref(tv), gathered, first, stride, n))
         if self._rec is not None:
             self._rec["fold"].append(((tv, [(None, sid)]), first, stride, n))
+
+    def _p2p_fold(self, epoch: int, counts, ops) -> None:
+        """Wait for the board slot of ``epoch`` and apply the fold ops in order: one kernel
+        (dk_p2p_wait_fold) when every target is a scalar, else the wait then dk_accum per op."""
+        if len(ops) <= runtime.P2P_FOLDS and all(tv.rank == 0 for tv, *_ in ops):
+            n = len(ops)
+            check(self.lib.dk_p2p_wait_fold(
+                epoch, counts, n, (c_uint64 * max(n, 1))(*[tv.ptr for tv, *_ in ops]),
+                (c_int64 * max(n, 1))(*[o[1] for o in ops]), (c_int64 * max(n, 1))(*[o[2] for o in ops]),
+                (c_int32 * max(n, 1))(*[o[3] for o in ops])))
+            return
+        g = c_uint64()
+        check(self.lib.dk_p2p_wait(epoch, counts, byref(g)))
+        for tv, first, stride, n in ops:
+            check(self.lib.dk_accum(byref(tv), g.value, first, stride, n))
 
     def _fold(self, task, kp, prank, rects, red_targets, gathered, maxp, nred) -> None:
         """Fold gathered per-point totals ([world][maxp][nred]) in lexicographic point order."""

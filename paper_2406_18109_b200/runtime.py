@@ -108,6 +108,10 @@ _SIGS = {
     "dk_timestamp": (c_int, [c_uint64, c_int64]),
     "dk_launch_pub": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_int64, c_int]),
     "dk_p2p_wait": (c_int, [c_int64, POINTER(c_int32), POINTER(c_uint64)]),
+    "dk_p2p_wait_fold": (
+        c_int,
+        [c_int64, POINTER(c_int32), c_int, POINTER(c_uint64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32)],
+    ),
     "dk_dma_send": (c_int, [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
     "dk_dma_recv": (c_int, [c_int, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
     "dk_p2p_exchange": (
@@ -121,6 +125,7 @@ P2P_SLOTS = 4
 P2P_POINTS = 16
 P2P_RED = 32
 P2P_MAIL_BYTES = 1 << 20
+P2P_FOLDS = 64
 
 EXPORTED = tuple(_SIGS)
 

@@ -583,6 +583,22 @@ class FakeLib:
         self.p2p_nred[slot] = nred
         return self.dk_launch(h, views, nviews, scalars, nscal, self.board_ptr + off)
 
+    def dk_p2p_wait_fold(self, epoch, counts, nfold, targets, firsts, strides, ns):
+        g = ctypes.c_uint64()
+        rc = self.dk_p2p_wait(epoch, counts, ctypes.byref(g))
+        if rc:
+            return rc
+        gb, goff = self._resolve(g.value)
+        garr = gb[goff:].view(np.float64)
+        for i in range(nfold):
+            tb, toff = self._resolve(targets[i])
+            t = tb[toff:toff + 8].view(np.float64)
+            a = float(t[0])
+            for k in range(ns[i]):
+                a = a + float(garr[firsts[i] + k * strides[i]])
+            t[0] = a
+        return 0
+
     def dk_p2p_wait(self, epoch, counts, ref):
         import torch
         import torch.distributed as dist
