@@ -26,6 +26,7 @@ import subprocess
 import sys
 import threading
 import time
+import types
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -130,7 +131,7 @@ class ClockSampler:
 # CPU samples of the reference path: the unmodified diffusekit.Session (numpy executor) on
 # the same task streams at a bounded size (per GPU-config unit counts in WORKLOADS)
 REF_SAMPLE = {
-    "bs": ("gen_blackscholes_chain(size=1_000_000, nodes=1)", 1_000_000),
+    "bs": ("gen_blackscholes_chain(size=10_000_000, nodes=1)", 10_000_000),
     "stencil": ("stencil_bands(8192, 1): 8192^2 interior + residual", 8192 ** 2),
     "cg": ("cg_csr(4096, 4096, 1): 2-D Poisson CSR, 16.8M rows", 4096 ** 2),
     "pcg": ("pcg_csr(4096, 4096, 1): Jacobi-PCG, 16.8M rows", 4096 ** 2),
@@ -143,7 +144,7 @@ def _ref_events(wl, iters):
     import workloads as W  # harness generators (the reference's own trace events; tools/workloads.py)
 
     if wl == "bs":
-        return W.blackscholes(1_000_000, 1, iters)[0], {}, None
+        return W.blackscholes(REF_SAMPLE["bs"][1], 1, iters)[0], {}, None
     if wl == "stencil":
         ev, init, _ = W.stencil_bands(8192, 1, iters)
     elif wl == "cg":
@@ -671,15 +672,23 @@ def e2e_bs(ex, trace, steps, torch, ext_stream, world):
     lo, hi = min(r[0][0] for r in mine), max(r[1][0] for r in mine)
     rect = ((lo,), (hi,))
     n = hi - lo
+    # pinned host memory for this rank's band only; the copies address it with global element
+    # offsets (store-shaped views), so each buffer is handed over with its base shifted by -lo
     ptrs = []
     for _ in range(3):
         p = ctypes.c_void_p()
-        check(ex.lib.dk_host_alloc(8 * int(np.prod(shape)), ctypes.byref(p)))
+        check(ex.lib.dk_host_alloc(8 * n, ctypes.byref(p)))
         ptrs.append(p)
-    hx, hy, ho = (np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=shape) for p in ptrs)
+    bx, by, bo = (np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(n,)) for p in ptrs)
+
+    class _Band:  # .ctypes.data = address of global element 0 (never dereferenced outside [lo, hi))
+        def __init__(self, band):
+            self.ctypes = types.SimpleNamespace(data=band.ctypes.data - 8 * lo)
+
+    hx, hy, ho = _Band(bx), _Band(by), _Band(bo)
     rng = np.random.default_rng(1)
-    hx[lo:hi] = rng.integers(1, 10, size=n)
-    hy[lo:hi] = rng.integers(1, 10, size=n)
+    bx[:] = rng.integers(1, 10, size=n)
+    by[:] = rng.integers(1, 10, size=n)
     from paper_2406_18109_b200.streaming import HostStreamer
 
     streamer = HostStreamer(ex, chunks=16) if len(execs) == 1 else None
@@ -702,7 +711,7 @@ def e2e_bs(ex, trace, steps, torch, ext_stream, world):
     ex.sync()
     ms = start.elapsed_time(end)
     # the chain's operator cycle is the identity: out == x + y exactly
-    ok = bool(np.array_equal(ho[lo:hi], hx[lo:hi] + hy[lo:hi]))
+    ok = bool(np.array_equal(bo, bx + by))
     for p in ptrs:
         check(ex.lib.dk_host_free(p))
     return ms, 16 * n, 8 * n, ok
@@ -771,7 +780,9 @@ def run_gpusession(steps, rank, world, local, size=1_000_000_000, graphs=True, e
             rng = np.random.default_rng(1)
             hx[:] = rng.integers(1, 10, size=n)
             hy[:] = rng.integers(1, 10, size=n)
+            s.stream_out(2, ho)  # the window writing out copies it back while it runs
             host = (hx, hy, ho)
+            streamed0 = s.streamed_windows
         gs0 = dict(s.executor.graph_stats)
         t0 = time.perf_counter()
         for it in its[n_it - steps:]:
@@ -790,8 +801,11 @@ def run_gpusession(steps, rank, world, local, size=1_000_000_000, graphs=True, e
             out["h2d_bytes_per_step"] = 16 * size
             out["d2h_bytes_per_step"] = 8 * size
             out["result_check"] = "out == x + y" if np.array_equal(host[2], host[0] + host[1]) else "FAILED"
-            out["path"] = ("GpuSession: heap.arrays[x], heap.arrays[y] = pinned host arrays; submit/flush the "
-                           "67-task iteration; heap.get(out, out=pinned)")
+            out["streamed_windows"] = s.streamed_windows - streamed0
+            out["path"] = ("GpuSession (drop-in): heap.arrays[x], heap.arrays[y] = pinned host arrays; "
+                           "submit/flush the 67-task iteration -- the window reading them runs host-streamed "
+                           "(H2D / kernel / D2H of stream_out(out) in 16 chunks over 3 streams); "
+                           "heap.get(out, out=pinned)")
         out["note"] = ("wall clock: reference front end (window analysis, memo replay, report) + GpuSession "
                        "execution")
         return out
@@ -1033,6 +1047,14 @@ def run_ours(args):
                 out[key] = run_gpusession(kw.pop("steps", args.steps), rank, world, local, warmup=args.warmup, **kw)
             except Exception as exc:  # noqa: BLE001
                 out[key] = {"error": f"{type(exc).__name__}: {exc}"}
+    ge = out.get("gpusession_e2e")
+    if isinstance(ge, dict) and ge.get("result_check") == "out == x + y" and "e2e" in out:
+        # the headline end-to-end number goes through the drop-in API; the executor-level
+        # streamer number stays beside it
+        out["e2e_executor"] = out["e2e"]
+        out["e2e"] = {"value": ge["value"], "unit": "iter/s", "h2d_bytes_per_step": ge["h2d_bytes_per_step"],
+                      "d2h_bytes_per_step": ge["d2h_bytes_per_step"], "path": ge["path"],
+                      "result_check": ge["result_check"], "timing": "wall clock, reference front end included"}
     if rank == 0 and world == 1 and not args.quick:
         try:
             out["cpu_baseline"] = run_cpu_baseline(wl, "fused")

@@ -38,6 +38,16 @@ class _Arrays:
 
     def __setitem__(self, sid: int, value) -> None:
         a = np.asarray(value, dtype=np.float64)
+        sess = self._heap.session
+        if sess is not None and sess._is_pinned(a):
+            # a pinned host array: the store's contents are defined now, the copy is
+            # made by the first window that reads it (streamed with its kernel)
+            sess._host_in[sid] = a
+            sess._out_fresh.discard(sid)
+            return
+        if sess is not None:
+            sess._host_in.pop(sid, None)
+            sess._out_fresh.discard(sid)
         self._heap.ex.upload(sid, a)
 
     def __getitem__(self, sid: int) -> np.ndarray:
@@ -59,21 +69,45 @@ class _Arrays:
 class GpuHeap:
     """Reference ``Heap`` API over device-resident stores."""
 
-    def __init__(self, executor: Executor) -> None:
+    def __init__(self, executor: Executor, session: "GpuSession | None" = None) -> None:
         self.ex = executor
+        self.session = session
         self.arrays = _Arrays(self)
 
     def get(self, store_id: int, out: np.ndarray | None = None) -> np.ndarray:
         """The store's contents (``Heap.get``); ``out`` (backend extension): copy into this
-        full-store array instead of a new one -- pinned memory makes the copy a DMA."""
+        full-store array instead of a new one -- pinned memory makes the copy a DMA.  A store
+        a streamed window already copied back into ``out`` (``GpuSession.stream_out``) is
+        not copied again."""
+        sess = self.session
+        if sess is not None:
+            host = sess._host_in.get(store_id)
+            if host is not None:
+                if out is None:
+                    return np.array(host, copy=True)
+                out[...] = host
+                return out
+            if store_id in sess._out_fresh:
+                self.ex.sync()
+                host = sess._host_out[store_id]
+                if out is None:
+                    return np.array(host, copy=True)
+                if out is not host:
+                    out[...] = host
+                return out
         if out is not None:
             return self.ex.download(store_id, out=out)
         return self.ex.get(store_id)
 
     def materialized(self, store_id: int) -> bool:
+        if self.session is not None and store_id in self.session._host_in:
+            return True
         return self.ex.materialized(store_id)
 
     def free(self, store_id: int) -> None:
+        if self.session is not None:
+            self.session._host_in.pop(store_id, None)
+            self.session._out_fresh.discard(store_id)
         self.ex.free(store_id)
 
     def digest(self, ids: Sequence[int]) -> dict[int, bytes]:
@@ -94,7 +128,14 @@ class GpuSession(_RefSession):
     ``graphs`` (default on, one GPU): launch segments that repeat -- the
     windows of a flush that all hit the launch-plan cache with identical
     bindings, as memo replays of a steady iteration do -- are relaunched as one
-    CUDA graph (``Executor.drain``); ``DK_GRAPHS=0`` turns it off."""
+    CUDA graph (``Executor.drain``); ``DK_GRAPHS=0`` turns it off.
+
+    Host-streamed windows (one GPU): a store assigned a pinned host array
+    (``heap.arrays[sid] = session.pinned(...)``) is not uploaded at once; the
+    first window that reads it -- if it is element-wise over rank-1 views --
+    runs through :class:`streaming.HostStreamer`, its H2D copies, kernel and the
+    D2H copies of stores registered with :meth:`stream_out` pipelined in chunks
+    over three streams.  Any other use uploads first."""
 
     def __init__(self, config=None, registry=None, builtins=None, *, rank=0, world=1, device=None,
                  init=None, dtypes=None, graphs=True):
@@ -108,10 +149,62 @@ class GpuSession(_RefSession):
             device=device,
             shape_of=lambda sid: self.stores[sid].shape.extents,
         )
-        self.heap = GpuHeap(self.executor)
+        self.heap = GpuHeap(self.executor, self)
         self._lowered: dict[int, tuple[object, object]] = {}
         self._pinned: list = []
+        self._pinned_ranges: list[tuple[int, int]] = []
+        self._host_in: dict[int, np.ndarray] = {}  # pinned host contents not yet copied to the device
+        self._host_out: dict[int, np.ndarray] = {}  # stream_out registrations
+        self._out_fresh: set[int] = set()  # stores whose _host_out copy is current
+        self._streamer = None
+        self.streamed_windows = 0
         self.executor.enable_graphs(graphs)
+
+    def stream_out(self, store_id: int, host: np.ndarray) -> None:
+        """Register a pinned full-store array that streamed windows writing ``store_id`` copy
+        their result into (``heap.get(store_id, out=host)`` then needs no further copy)."""
+        if not self._is_pinned(host):
+            raise ValueError("stream_out needs an array from GpuSession.pinned()")
+        self._host_out[store_id] = host
+
+    def _is_pinned(self, a: np.ndarray) -> bool:
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+            return False
+        lo = a.ctypes.data
+        return any(b <= lo and lo + a.nbytes <= e for b, e in self._pinned_ranges)
+
+    def _materialize_host(self, sids) -> None:
+        for sid in sids:
+            host = self._host_in.pop(sid, None)
+            if host is not None:
+                self.executor.upload(sid, host)
+
+    def _try_stream(self, task, kp, temp_positions) -> bool:
+        """Run the window through the host streamer if it reads pending host inputs and can be."""
+        ins = {a.store for j, a in enumerate(task.args) if j not in temp_positions and a.store in self._host_in}
+        if not ins:
+            return False
+        writes = {a.store for j, a in enumerate(task.args) if j not in temp_positions and a.writes}
+        if (kp is None or self.executor.world != 1 or ins & writes or any(a.reduces for a in task.args)
+                or any(len(self.stores[a.store].shape.extents) != 1
+                       for j, a in enumerate(task.args) if j not in temp_positions)):
+            return False
+        from .errors import UnsupportedError
+        from .streaming import HostStreamer
+
+        if self._streamer is None:
+            self._streamer = HostStreamer(self.executor, chunks=16)
+        outs = {sid: self._host_out[sid] for sid in writes if sid in self._host_out}
+        try:
+            self._streamer.run(task, kp, temp_positions, {sid: self._host_in[sid] for sid in ins}, outs)
+        except UnsupportedError:
+            return False
+        for sid in ins:
+            del self._host_in[sid]
+        self._out_fresh.difference_update(writes)
+        self._out_fresh.update(outs)
+        self.streamed_windows += 1
+        return True
 
     def _flush(self, explicit: bool) -> None:  # pipeline.py:194-240, unchanged; then end the launch segment
         try:
@@ -121,6 +214,9 @@ class GpuSession(_RefSession):
 
     def close(self) -> None:
         """Release the device stores, graphs and pinned host buffers of this session."""
+        self._host_in.clear()
+        self._host_out.clear()
+        self._out_fresh.clear()
         self.executor.close()
         for p in self._pinned:
             self.executor.lib.dk_host_free(p)
@@ -132,6 +228,7 @@ class GpuSession(_RefSession):
 
         a, p = pinned(self.executor, tuple(shape), dtype)
         self._pinned.append(p)
+        self._pinned_ranges.append((a.ctypes.data, a.ctypes.data + a.nbytes))
         return a
 
     def _lower(self, kernel, fused: bool):
@@ -164,7 +261,15 @@ class GpuSession(_RefSession):
             # arena-combined reductions on the device path
             isolated = plan.f > 1 and self.config.isolated
             try:
-                self.executor.execute(lower_task(plan.task), kp, plan.temp_positions, isolated=isolated)
+                task = lower_task(plan.task)
+                streamed = False
+                if self._host_in:
+                    streamed = not isolated and self._try_stream(task, kp, plan.temp_positions)
+                    if not streamed:
+                        self._materialize_host({a.store for a in task.args})
+                if not streamed:
+                    self._out_fresh.difference_update({a.store for a in task.args if a.writes or a.reduces})
+                    self.executor.execute(task, kp, plan.temp_positions, isolated=isolated)
             except UnknownTaskKind as e:
                 raise _ref_exec.UnknownTaskKindError(str(e)) from e
             except ArenaViolation as e:

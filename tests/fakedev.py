@@ -488,6 +488,32 @@ class FakeLib:
                 self.xrecv[q] = self.xrecv.get(q, 0) + 1
         return self.dk_comm_exchange(n, sids, peers, dirs, los, his)
 
+    # pinned host memory and raw copies (HostStreamer)
+    def dk_host_alloc(self, nbytes, ref):
+        buf = np.zeros(max(int(nbytes), 16), dtype=np.uint8)
+        self._host_bufs = getattr(self, "_host_bufs", {})
+        self._host_bufs[buf.ctypes.data] = buf
+        ref._obj.value = buf.ctypes.data
+        return 0
+
+    def dk_host_free(self, p):
+        addr = p.value if hasattr(p, "value") else int(p)
+        getattr(self, "_host_bufs", {}).pop(addr, None)
+        return 0
+
+    def _host_bytes(self, addr, n):
+        return np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(int(addr)))
+
+    def dk_memcpy_h2d(self, dptr, host, nbytes):
+        buf, off = self._resolve(dptr)
+        buf[off:off + nbytes] = self._host_bytes(host, nbytes)
+        return 0
+
+    def dk_memcpy_d2h_async(self, host, dptr, nbytes):
+        buf, off = self._resolve(dptr)
+        self._host_bytes(host, nbytes)[:] = buf[off:off + nbytes]
+        return 0
+
     # streams / events: the stand-in executes every call at once, in call order
     def dk_stream_new(self, ref):
         _set(ref, 1000 + getattr(self, "_nstreams", 0))

@@ -232,3 +232,72 @@ def test_spmv_dot_epilogue_matches_reference(name):
     for s, want in golden_arrays(case).items():
         got = ex.get(s)
         np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(want)))))
+
+
+def test_host_streamed_windows_in_gpusession(monkeypatch):
+    """GpuSession streams a window whose inputs were assigned pinned host arrays: H2D, kernel and the
+    D2H of stream_out stores in chunks (CPU stand-in); the results equal the reference Session's, and
+    the e2e loop (assign x, y; flush; get out) returns out == x + y every iteration."""
+    import sys
+
+    from conftest import reference_available
+
+    ref_src = reference_available()
+    if ref_src is None:
+        pytest.skip("reference not importable")
+    if ref_src not in sys.path:
+        sys.path.insert(0, ref_src)
+    from diffusekit.pipeline import Session, SessionConfig, run_events, task_from_event
+    from diffusekit.trace import CreatePartition, CreateStore, DropRef, Flush, TaskEvent, gen_blackscholes_chain, \
+        partition_from_event
+    from fakedev import FakeLib
+
+    from paper_2406_18109_b200 import runtime
+    from paper_2406_18109_b200.session import GpuSession
+
+    monkeypatch.setattr(runtime, "load", lambda *a, **k: FakeLib(0, 1, device_model=True))
+    monkeypatch.setenv("DK_HOST_INIT", "1")
+    n = 1000
+    ev = gen_blackscholes_chain(size=n, nodes=1, iters=8)
+    its, cur = [], []
+    for e in ev:
+        cur.append(e)
+        if isinstance(e, Flush):
+            its.append(cur)
+            cur = []
+    s = GpuSession(SessionConfig())
+    ref = Session(SessionConfig())
+
+    def feed(sess, evs):
+        for e in evs:
+            if isinstance(e, CreateStore):
+                sess.create_store(e.id, e.shape)
+            elif isinstance(e, CreatePartition):
+                sess.create_partition(e.id, partition_from_event(e))
+            elif isinstance(e, TaskEvent):
+                sess.submit(task_from_event(sess, e))
+            elif isinstance(e, DropRef):
+                sess.drop_ref(e.store)
+            else:
+                sess.flush()
+
+    hx, hy, ho = s.pinned((n,)), s.pinned((n,)), s.pinned((n,))
+    s.stream_out(2, ho)
+    rng = np.random.default_rng(5)
+    for k, it in enumerate(its):
+        feed(s, [e for e in it if isinstance(e, (CreateStore, CreatePartition))])
+        feed(ref, [e for e in it if isinstance(e, (CreateStore, CreatePartition))])
+        hx[:] = rng.integers(1, 10, n)
+        hy[:] = rng.integers(1, 10, n)
+        s.heap.arrays[0] = hx
+        s.heap.arrays[1] = hy
+        ref.heap.arrays[0] = hx.copy()
+        ref.heap.arrays[1] = hy.copy()
+        feed(s, [e for e in it if not isinstance(e, (CreateStore, CreatePartition))])
+        feed(ref, [e for e in it if not isinstance(e, (CreateStore, CreatePartition))])
+        got = s.heap.get(2, out=ho)
+        assert got is ho and np.array_equal(ho, hx + hy), k
+        assert np.array_equal(s.heap.get(2), ref.heap.get(2))
+        assert np.array_equal(s.heap.get(0), hx)
+    assert s.streamed_windows >= 5, s.streamed_windows
+    s.close()
