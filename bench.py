@@ -487,20 +487,20 @@ def measure(ex, trace, steps, warmup, torch, ext_stream, rank, with_events=True,
     its, steady = iteration_split(trace)
     seq = list(range(steady)) + [steady + (i % (len(its) - steady)) for i in range(warmup + steps)]
     cycled = len(seq) > len(its)
+    trace_ts = os.environ.get("DK_TRACE_TS") == "1"
+    if trace_ts:
+        ex.trace_timestamps()
+    # no cyclic-GC pauses inside the warm-up or the timed region (earlier workloads' traces
+    # leave millions of objects for a full collection to walk).  Collected before the
+    # warm-up: a collection between the warm-up and the start barrier left the GPUs idle
+    # long enough to come out of their boost clocks (first timed iteration +0.5 ms on 4 GPUs)
+    gc.collect()
+    gc.disable()
     for i in seq[: steady + warmup]:
         if cycled:
             fresh_targets(ex, trace, its[i])
         replay(ex, its[i])
     ex.sync()
-    # no cyclic-GC pauses inside the timed region (earlier workloads' traces
-    # leave millions of objects for a full collection to walk); collected before
-    # the barrier, so no rank starts its timed region a collection late
-    trace_ts = os.environ.get("DK_TRACE_TS") == "1"
-    if trace_ts:
-        ex.trace_timestamps()
-        ex.sync()
-    gc.collect()
-    gc.disable()
     if sync_ranks is not None:
         sync_ranks()  # every rank starts its timed region together (warm-up lengths differ)
     timed = seq[steady + warmup:]

@@ -301,3 +301,26 @@ def test_host_streamed_windows_in_gpusession(monkeypatch):
         assert np.array_equal(s.heap.get(0), hx)
     assert s.streamed_windows >= 5, s.streamed_windows
     s.close()
+
+
+def test_builtin_input_overlapping_its_output_is_copied_in():
+    """MATVEC whose vector operand and result are overlapping views of one store: numpy computes
+    ``a0 @ a1`` before assigning (executor.py:93-94); the executor reads a copy."""
+    from fakedev import FakeLib
+
+    from paper_2406_18109_b200.executor import Executor
+    from paper_2406_18109_b200.ir import ArgDesc, PartDesc, TaskDesc
+
+    ex = Executor(shapes={0: (6, 6), 1: (8,)}, lib=FakeLib(0, 1, device_model=True))
+    A = np.arange(36.0).reshape(6, 6) / 7.0
+    v = np.arange(1.0, 9.0)
+    ex.upload(0, A)
+    ex.upload(1, v)
+    whole = PartDesc("tiling", (6, 6), (0, 0), ((1,), (1,)), (0, 0))
+    xin = PartDesc("tiling", (6,), (0,), ((1,),), (0,))
+    yout = PartDesc("tiling", (6,), (2,), ((1,),), (0,))
+    task = TaskDesc("MATVEC", (1,), (ArgDesc(0, whole, "R"), ArgDesc(1, xin, "R"), ArgDesc(1, yout, "W")))
+    ex.execute(task, None)
+    want = v.copy()
+    want[2:8] = A @ v[0:6]
+    assert np.allclose(ex.get(1), want, rtol=1e-15)
