@@ -318,7 +318,46 @@ __global__ void k_matvec(dk_view A, dk_view xv, dk_view yv) {
   }
 }
 
-// ---- NORM: target += sum(x*x), single block, fixed order ---------------------
+// ---- NORM: target += sum(x*x) --------------------------------------------------
+// Grid-wide and deterministic: CTA b sums its contiguous element range
+// (thread-strided, warp shuffle tree, fixed smem tree) into parts[b]; one
+// thread then folds parts[0..G) in order and adds the total.  G depends only
+// on n and the SM count.
+
+__global__ void __launch_bounds__(256) k_norm_part(dk_view xv, double* parts, int64_t per_cta) {
+  __shared__ double sh[8];
+  int64_t n = 1;
+  for (int d = 0; d < xv.rank; ++d) n *= xv.ext[d];
+  const double* x = (const double*)xv.ptr;
+  const int64_t lo = (int64_t)blockIdx.x * per_cta, hi = lo + per_cta < n ? lo + per_cta : n;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double v = x[VIdx::off(xv, i)];
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s = __dadd_rn(s, sh[w]);
+    parts[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_norm_fold(dk_view t, const double* parts, int nparts) {
+  double s = 0.0;
+  for (int b = 0; b < nparts; ++b) s = __dadd_rn(s, parts[b]);
+  int64_t nt = 1;
+  for (int d = 0; d < t.rank; ++d) nt *= t.ext[d];
+  double* tp = (double*)t.ptr;
+  for (int64_t i = 0; i < nt; ++i) {
+    double* q = tp + VIdx::off(t, i);
+    *q = __dadd_rn(*q, s);
+  }
+}
+
+// single-block variant (DK_NORM_ONEBLOCK=1): round 1's kernel
 
 __global__ void k_norm(dk_view xv, dk_view t) {
   __shared__ double sh[32];
@@ -453,9 +492,25 @@ void launch_builtin(const std::string& kind, const dk_view* v, int n, const int3
     if (n != 2) fail(DK_ERR_ARG, "NORM expects 2 args");
     check_f64(v[0], "NORM");
     check_f64(v[1], "NORM");
-    k_norm<<<1, 1024, 0, s>>>(v[0], v[1]);
+    static const bool one = getenv("DK_NORM_ONEBLOCK") != nullptr;
+    const int64_t cnt = view_volume(v[0]);
+    if (one || cnt < (1 << 16)) {
+      k_norm<<<1, 1024, 0, s>>>(v[0], v[1]);
+      DK_CUDA(cudaGetLastError());
+      st().launches++;
+      return;
+    }
+    const int64_t want = (cnt + 256 * 16 - 1) / (256 * 16);
+    const int g = (int)std::min<int64_t>(want, (int64_t)sms * 4);
+    const int64_t per = (cnt + g - 1) / g;
+    double* parts = nullptr;
+    DK_CUDA(cudaMallocAsync((void**)&parts, sizeof(double) * g, s));
+    k_norm_part<<<g, 256, 0, s>>>(v[0], parts, per);
     DK_CUDA(cudaGetLastError());
-    st().launches++;
+    k_norm_fold<<<1, 1, 0, s>>>(v[1], parts, g);
+    DK_CUDA(cudaGetLastError());
+    DK_CUDA(cudaFreeAsync(parts, s));
+    st().launches += 2;
     return;
   }
   if (kind == "OPAQUE") {

@@ -310,3 +310,29 @@ def test_spmv_dot_epilogue_golden(Executor, bench_cases):
         finally:
             ex.close()
     assert n >= 3
+
+
+def test_norm_builtin_grid_wide(Executor):
+    """NORM (acc += sum(x*x), executor.py:97-98) on 3M elements: the grid-wide deterministic kernel
+    (per-CTA partials folded in order) against numpy, accumulating onto the target's contents, and
+    run-to-run bit-identical."""
+    from paper_2406_18109_b200.ir import NONE_PART, ArgDesc, PartDesc, TaskDesc
+
+    n = 3_000_001
+    x = np.random.default_rng(11).random(n) - 0.25
+    full = PartDesc("tiling", (n,), (0,), ((1,),), (0,))
+    res = []
+    for _ in range(2):
+        ex = Executor(shapes={0: (n,), 1: ()}, device=0)
+        try:
+            ex.upload(0, x)
+            ex.upload(1, np.array(2.5))
+            task = TaskDesc("NORM", (1,), (ArgDesc(0, full, "R"), ArgDesc(1, NONE_PART, "Rd")))
+            ex.execute(task, None)
+            ex.execute(task, None)
+            res.append(float(ex.get(1)[()]))
+        finally:
+            ex.close()
+    want = 2.5 + 2 * float(np.sum(x * x))
+    assert abs(res[0] - want) <= 1e-12 * want
+    assert res[0] == res[1]
