@@ -38,14 +38,39 @@ def _run(Executor, trace, world=1):
         ex.close()
 
 
-def _compare(name, got, want, exact):
+def _compare(name, got, want, exact, trace=None):
+    """``exact``: every store bit-identical.  Otherwise stores a reduction result can reach
+    (``_reduction_reach``) within rtol 1e-12 -- a reduction's summation order differs from
+    np.sum -- and every other store still bit-identical (no FMA, IEEE-exact elementwise ops)."""
+    reach = _reduction_reach(trace) if (trace is not None and not exact) else None
     for s, w in want.items():
         g = got[s]
-        if exact:
+        if exact or (reach is not None and s not in reach):
             assert same_bits(g, w), f"{name}: store {s} not bit-identical"
         else:
             np.testing.assert_allclose(g, w, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(w)))),
                                        err_msg=f"{name}: store {s}")
+
+
+def _reduction_reach(trace):
+    """Stores whose final contents can depend on a reduction result: the reduction targets and,
+    transitively, every store written by a launch that reads a reached store."""
+    reach = set()
+    changed = True
+    execs = trace.execs()
+    while changed:
+        changed = False
+        for e in execs:
+            args = [a for j, a in enumerate(e.task.args) if j not in e.temp_positions]
+            new = {a.store for a in args if a.reduces}
+            # a launch (a fused window included: its demoted temporaries stay inside it) that reads
+            # a reached store can pass it on to everything it writes
+            if any(a.reads and a.store in reach for a in args):
+                new |= {a.store for a in args if a.writes or a.reduces}
+            if not new <= reach:
+                reach |= new
+                changed = True
+    return reach
 
 
 def _integer_valued(arrs):
@@ -62,7 +87,7 @@ def test_golden_bench_cases(Executor, bench_cases):
         want = golden_arrays(case)
         exact = _integer_valued(want)
         exact_cases += exact
-        _compare(case["name"], got, want, exact)
+        _compare(case["name"], got, want, exact, trace)
     assert exact_cases >= 5
 
 
@@ -73,7 +98,7 @@ def test_golden_fuzz_corpus(Executor, fuzz_cases):
         trace = PlanTrace.from_json(case["trace"])
         got, _ = _run(Executor, trace)
         want = golden_arrays(case)
-        _compare(case["name"], got, want, _integer_valued(want))
+        _compare(case["name"], got, want, _integer_valued(want), trace)
 
 
 def test_medium_plans_match_oracle(Executor):
@@ -87,11 +112,9 @@ def test_medium_plans_match_oracle(Executor):
         ref = oracle_replay(tr)
         want = {s: ref.get(s) for s in tr.live}
         name = tr.meta.get("name", "?")
-        exact = name.startswith(("bs_", "stencil_")) and _integer_valued(want)
-        if name.startswith("stencil"):
-            # residual DOTs sum non-integers in a different order than np.sum
-            exact = False
-        _compare(name, got, want, exact)
+        # integer-valued heaps bit-exact throughout; otherwise only what a reduction result
+        # reaches is compared at rtol (the stencil's res histories; CG's vectors via pq / rs)
+        _compare(name, got, want, _integer_valued(want), tr)
 
 
 _VARIANT_SCRIPT = r"""
@@ -111,7 +134,7 @@ for tr in traces:
         continue
     got, _ = T._run(Executor, tr)
     ref = oracle_replay(tr)
-    T._compare(name, got, {s: ref.get(s) for s in tr.live}, False)
+    T._compare(name, got, {s: ref.get(s) for s in tr.live}, False, tr)
     n += 1
 print("checked", n)
 """
