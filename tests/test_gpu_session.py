@@ -131,3 +131,60 @@ def test_heap_arrays_injection(dk):
         assert s.heap.get(2)[()] == 16.0
     finally:
         s.executor.close()
+
+
+def test_host_streamed_iterations(dk):
+    """The e2e path: pinned x, y assigned through heap.arrays, the window reading them runs
+    host-streamed (chunked H2D / kernel / D2H of stream_out(out)), results equal the reference
+    Session's on the same inputs every iteration."""
+    from diffusekit.pipeline import Session, SessionConfig, task_from_event
+    from diffusekit.trace import CreatePartition, CreateStore, DropRef, Flush, TaskEvent, gen_blackscholes_chain, \
+        partition_from_event
+
+    from paper_2406_18109_b200.session import GpuSession
+
+    n = 1 << 20
+    its, cur = [], []
+    for e in gen_blackscholes_chain(size=n, nodes=1, iters=6):
+        cur.append(e)
+        if isinstance(e, Flush):
+            its.append(cur)
+            cur = []
+
+    def feed(sess, evs):
+        for e in evs:
+            if isinstance(e, CreateStore):
+                sess.create_store(e.id, e.shape)
+            elif isinstance(e, CreatePartition):
+                sess.create_partition(e.id, partition_from_event(e))
+            elif isinstance(e, TaskEvent):
+                sess.submit(task_from_event(sess, e))
+            elif isinstance(e, DropRef):
+                sess.drop_ref(e.store)
+            else:
+                sess.flush()
+
+    s = GpuSession(SessionConfig(), device=0)
+    ref = Session(SessionConfig())
+    try:
+        hx, hy, ho = s.pinned((n,)), s.pinned((n,)), s.pinned((n,))
+        s.stream_out(2, ho)
+        rng = np.random.default_rng(3)
+        for k, it in enumerate(its):
+            head = [e for e in it if isinstance(e, (CreateStore, CreatePartition))]
+            body = [e for e in it if not isinstance(e, (CreateStore, CreatePartition))]
+            feed(s, head)
+            feed(ref, head)
+            hx[:] = rng.integers(1, 10, n)
+            hy[:] = rng.random(n)
+            s.heap.arrays[0] = hx
+            s.heap.arrays[1] = hy
+            ref.heap.arrays[0] = hx.copy()
+            ref.heap.arrays[1] = hy.copy()
+            feed(s, body)
+            feed(ref, body)
+            assert s.heap.get(2, out=ho) is ho
+            assert same_bits(ho, ref.heap.get(2)), k
+        assert s.streamed_windows >= len(its)
+    finally:
+        s.close()
