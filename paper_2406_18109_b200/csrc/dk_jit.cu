@@ -1079,13 +1079,38 @@ class Gen {
     o << "    #pragma unroll\n    for (int u = 0; u < " << kTR / 4 << "; ++u) {\n";
     o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
     o << "      if (row < D0 && e < D1) {\n        const bool full = e + 1 < D1;\n";
+    // an odd-column staged view whose left and right neighbour columns (same row) are
+    // staged even-column views is assembled from their registers (W.y, E.x) instead of
+    // two more shared-memory loads: the stencil's centre from its west and east views.
+    // Source views then always load both elements (in-bounds: the tile has halo columns).
+    static const bool no_reuse = getenv("DK_K3_NOREUSE") != nullptr;
+    std::vector<std::pair<int, int>> from(NS, {-1, -1});
+    std::vector<bool> is_src(NS, false);
+    auto scol = [&](int i) { return np.sites[i].dc - np.st_min_dc + np.st_sh; };
+    auto staged_loaded = [&](int i) { return np.sites[i].cls != 'S' && np.site_loaded[i] && np.sites[i].staged; };
+    if (!no_reuse)
+      for (int i = 0; i < NS; ++i) {
+        if (!staged_loaded(i) || scol(i) % 2 == 0) continue;
+        int l = -1, r = -1;
+        for (int j = 0; j < NS; ++j) {
+          if (!staged_loaded(j) || np.sites[j].dr != np.sites[i].dr) continue;
+          if (scol(j) == scol(i) - 1) l = j;
+          if (scol(j) == scol(i) + 1) r = j;
+        }
+        if (l >= 0 && r >= 0) {
+          from[i] = {l, r};
+          is_src[l] = is_src[r] = true;
+        }
+      }
     for (int i = 0; i < NS; ++i) {
       const Site& s = np.sites[i];
-      if (s.cls == 'S' || !np.site_loaded[i]) continue;
+      if (s.cls == 'S' || !np.site_loaded[i] || from[i].first >= 0) continue;
       if (s.staged) {
-        const int col = s.dc - np.st_min_dc + np.st_sh;  // tile column of element pair 0
+        const int col = scol(i);  // tile column of element pair 0
         o << "        { const double* t = &T[a + " << s.dr << "][2 * pr + " << col << "]; ";
-        if (col % 2 == 0)
+        if (col % 2 == 0 && is_src[i])
+          o << "v" << i << "[u] = *reinterpret_cast<const double2*>(t); }\n";
+        else if (col % 2 == 0)
           o << "v" << i << "[u] = full ? *reinterpret_cast<const double2*>(t) : make_double2(t[0], 0.0); }\n";
         else
           o << "v" << i << "[u].x = t[0]; v" << i << "[u].y = full ? t[1] : 0.0; }\n";
@@ -1097,6 +1122,10 @@ class Gen {
         o << ");\n";
       }
     }
+    for (int i = 0; i < NS; ++i)
+      if (from[i].first >= 0)
+        o << "        v" << i << "[u].x = v" << from[i].first << "[u].y; v" << i << "[u].y = v" << from[i].second
+          << "[u].x;\n";
     o << "      }\n    }\n";
     o << "    #pragma unroll\n    for (int u = 0; u < " << kTR / 4 << "; ++u) {\n";
     o << "      const int a = rg + 4 * u;\n      const int64_t row = r0 + a, e = c0 + 2 * pr;\n";
