@@ -140,7 +140,7 @@ print("checked", n)
 """
 
 
-@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT", "DK_JIT_PERSIST", "DK_K3_CYCLIC", "DK_K3_NOREUSE",
+@pytest.mark.parametrize("variant", ["DK_JIT_NO_K3", "DK_JIT_H", "DK_JIT_NO_SHIFT", "DK_JIT_PERSIST", "DK_K3_CYCLIC", "DK_K3_REUSE",
                                      "DK_K3_TR=12", "DK_K3_TR=16", "DK_K3S=1", "DK_K3_NOWS=1"])
 def test_stencil_codegen_variants_match_oracle(variant, tmp_path):
     """The stencil plans with the TMA-staged window (K3) off, the shuffled
