@@ -716,10 +716,21 @@ class Executor:
             return
         if any(sid not in cidx for sid, _ in rec["ensure"]) or any(sid not in cidx for sid, _ in rec["inits"]):
             return
+        ov = rec.get("overlap")
+        if ov is not None:
+            if any(sid not in cidx for sid, _r, _q in ov["sends"] + ov["recvs"]):
+                return
+            cvs = [canon_views(v, slots) for v, slots in ov["views"]]
+            if any(c is None for c in cvs):
+                return
+            plan["overlap"] = {"sends": [(cidx[sid], r, q) for sid, r, q in ov["sends"]],
+                               "recvs": [(cidx[sid], r, q) for sid, r, q in ov["recvs"]], "views": cvs}
         plan["views"], plan["fold"] = vs, fold
         dev = set()
         for item in vs:
             cv = item[0] if kp is None else item
+            dev.update(c for _, c, _ in cv[1])
+        for cv in plan.get("overlap", {}).get("views", ()):
             dev.update(c for _, c, _ in cv[1])
         for cv, *_ in fold:
             dev.update(c for _, c, _ in cv[1])
@@ -768,7 +779,13 @@ class Executor:
             self._exchange(n, (c_int64 * n)(*[sids[c] for c in cs]), peers, dirs, los, his)
             self.stats.transfers += n
             self.stats.bytes_moved += nbytes
-        if kp is None:
+        if kp is None and hit.get("overlap") is not None:
+            ov = hit["overlap"]
+            self._issue_spmv_overlap([(sids[c], r, q) for c, r, q in ov["sends"]],
+                                     [(sids[c], r, q) for c, r, q in ov["recvs"]],
+                                     [self._rebind(cv, bases) for cv in ov["views"]])
+            self.stats.bytes_moved += sum(rg.volume(r) * recs[c].esize for c, r, _q in ov["recvs"] + ov["sends"])
+        elif kp is None:
             kind = task.kind.encode()
             for cv, n, wflags in hit["views"]:
                 check(self.lib.dk_builtin(kind, self._rebind(cv, bases), n, wflags))
@@ -892,8 +909,6 @@ class Executor:
 
         mine = [i for i in range(V) if prank[i] == self.rank]
         if overlap:
-            if self._rec is not None:
-                self._rec["ok"] = False
             self._run_spmv_overlap(task, pts, mine, rects, lay, moves)
         elif kp is None:
             self._run_builtin(task, pts, mine, rects, prank)
@@ -962,22 +977,43 @@ class Executor:
     def _run_spmv_overlap(self, task, pts, mine, rects, lay, moves) -> None:
         t, nx = lay["t"], lay["nx"]
         i = mine[0]
-        r_rp, r_cl, r_vl, r_x, r_y = (self.stores[a.store] for a in task.args)
-        for rec, rect in zip((r_rp, r_cl, r_vl, r_x, r_y), rects[i]):
+        recs = [self.stores[a.store] for a in task.args]
+        for rec, rect in zip(recs, rects[i]):
             self._ensure(rec, rect)
+        r_rp, r_cl, r_vl, r_x, r_y = recs
+        rp0, y0 = rects[i][0][0][0], rects[i][4][0][0]
+
+        def rows(a, b):
+            views = (dk_view * 5)()
+            views[0] = self.view(r_rp, ((rp0 + a,), (rp0 + b + 1,)))
+            views[1] = self.view(r_cl, rects[i][1])
+            views[2] = self.view(r_vl, rects[i][2])
+            views[3] = self.view(r_x, r_x.full)
+            views[4] = self.view(r_y, ((y0 + a,), (y0 + b,)))
+            return views
+
+        launches = [rows(a, b) for a, b in ((nx, t - nx), (0, nx), (t - nx, t)) if b > a]
+        sends = [(x[0], x[1], x[3]) for x in moves if x[2] == self.rank]
+        recvs = [(x[0], x[1], x[2]) for x in moves if x[3] == self.rank]
+        if self._rec is not None:
+            slots = [(j, a.store) for j, a in enumerate(task.args)]
+            self._rec["overlap"] = {"sends": sends, "recvs": recvs, "views": [(v, slots) for v in launches]}
+        self._issue_spmv_overlap(sends, recvs, launches)
+
+    def _issue_spmv_overlap(self, sends, recvs, launches) -> None:
+        """Side stream: the halo sends (copy engine); main stream: the interior rows, the halo
+        receives, the boundary rows.  ``sends`` / ``recvs``: (store, rect, peer)."""
 
         def enc(lst):
             m = len(lst)
             sids = (c_int64 * max(m, 1))(*[x[0] for x in lst])
-            peers = (c_int32 * max(m, 1))(*[(x[3] if x[2] == self.rank else x[2]) for x in lst])
+            peers = (c_int32 * max(m, 1))(*[x[2] for x in lst])
             los = (c_int64 * (4 * max(m, 1)))()
             his = (c_int64 * (4 * max(m, 1)))()
             for k, x in enumerate(lst):
                 los[4 * k], his[4 * k] = x[1][0][0], x[1][1][0]
             return m, sids, peers, los, his
 
-        sends = [x for x in moves if x[2] == self.rank]
-        recvs = [x for x in moves if x[3] == self.rank]
         main = self.stream()
         if self._side is None:
             s = c_uint64()
@@ -998,27 +1034,14 @@ class Executor:
                 check(self.lib.dk_event_record(self._side_ev[1]))
             finally:
                 check(self.lib.dk_set_stream(main))
-        rp0, y0 = rects[i][0][0][0], rects[i][4][0][0]
         wflags = (c_int32 * 5)(0, 0, 0, 0, 1)
-
-        def rows(a, b):
-            if b <= a:
-                return
-            views = (dk_view * 5)()
-            views[0] = self.view(r_rp, ((rp0 + a,), (rp0 + b + 1,)))
-            views[1] = self.view(r_cl, rects[i][1])
-            views[2] = self.view(r_vl, rects[i][2])
-            views[3] = self.view(r_x, r_x.full)
-            views[4] = self.view(r_y, ((y0 + a,), (y0 + b,)))
-            check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
-
-        rows(nx, t - nx)  # interior: only this rank's own x rows
+        check(self.lib.dk_builtin(b"SPMV_CSR", launches[0], 5, wflags))  # interior: own x rows only
         self.mark("interior_done")
         if recvs:
             check(self.lib.dk_dma_recv(*enc(recvs)))
         self.mark("halo_in")
-        rows(0, nx)
-        rows(t - nx, t)
+        for views in launches[1:]:
+            check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
         if sends:
             check(self.lib.dk_stream_wait_event(self._side_ev[1]))  # p is not rewritten before the sends read it
         self.stats.p2p_halos += 1

@@ -214,6 +214,7 @@ def test_overlapped_halo_spmv_four_ranks():
     bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
     assert all(r[2] > 0 for r in res), res
+    assert all(r[3] > 0 for r in res), res  # steady iterations replay the recorded overlap plan
 
 
 def test_isolated_streams_two_ranks():
