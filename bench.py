@@ -962,6 +962,21 @@ def run_ours(args):
                       "d2h_bytes_per_step": bo,
                       "path": "streaming.HostStreamer: pinned H2D(x, y) / fused kernel / D2H(out) in 16 chunks over 3 streams",
                       "result_check": "out == x + y (the chain's operator cycle is the identity)" if ok else "FAILED"}
+    def spmv_dot_line(w2):
+        # opt-in SpMV + partial-dot epilogue (BASELINE configs[3] "fused SpMV+dot+axpy"): same plan,
+        # the [DOT, DOT] window's p.q comes from the SpMV kernel (at N > 1 through its peer-board block)
+        try:
+            e = one(w2, "fused", fuse_spmv_dot=True)
+            return {"iter_s": round(world * K / (e["ms"] / 1e3), 3), "ms_per_step": round(e["ms"] / K, 4),
+                    "ranks_ms_per_step": e["ranks_ms_per_step"],
+                    "per_exec_ms": e["dom"]["per_exec_ms"] if e["dom"] else None, "result_check": e["check"],
+                    "note": "DK_FUSE_SPMV_DOT=1: SPMV_CSR also emits per-CTA partials of p.q; the "
+                            "[DOT,DOT] window drops that reduction (2 x 0.537 GB less traffic per iteration)"}
+        except Exception as exc:  # noqa: BLE001
+            return {"error": f"{type(exc).__name__}: {exc}"}
+
+    if not args.no_extra and wl in ("cg", "pcg"):
+        out["fused_spmv_dot"] = spmv_dot_line(wl)
     if not args.no_extra:
         try:
             un = one(wl, "unfused")
@@ -991,20 +1006,8 @@ def run_ours(args):
                     "result_check": f["check"],
                     "unfused_result_check": u["check"],
                 }
-                if w2 in ("cg", "pcg") and world == 1:
-                    # opt-in SpMV + partial-dot epilogue (BASELINE configs[3] "fused SpMV+dot+axpy"):
-                    # same plan, the [DOT, DOT] window's p.q comes from the SpMV kernel
-                    try:
-                        e = one(w2, "fused", fuse_spmv_dot=True)
-                        others[w2]["fused_spmv_dot"] = {
-                            "iter_s": round(world * K / (e["ms"] / 1e3), 3),
-                            "ms_per_step": round(e["ms"] / K, 4),
-                            "per_exec_ms": e["dom"]["per_exec_ms"] if e["dom"] else None,
-                            "result_check": e["check"],
-                            "note": "DK_FUSE_SPMV_DOT=1: SPMV_CSR also emits per-CTA partials of p.q; the "
-                                    "[DOT,DOT] window drops that reduction (2 x 0.537 GB less traffic per iteration)"}
-                    except Exception as exc:  # noqa: BLE001
-                        others[w2]["fused_spmv_dot"] = {"error": f"{type(exc).__name__}: {exc}"}
+                if w2 in ("cg", "pcg"):
+                    others[w2]["fused_spmv_dot"] = spmv_dot_line(w2)
                 if rank == 0 and world == 1 and not args.quick:
                     try:
                         others[w2]["cpu_baseline"] = run_cpu_baseline(w2, "fused", budget_s=8.0)

@@ -186,6 +186,15 @@ int dk_p2p_init(int* enabled);
  * older or newer use of the slot. */
 int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
                   int64_t epoch, int point);
+/* dk_launch_pub whose point block holds nred_total totals of which the kernel writes
+ * its own at [red_offset, red_offset + its reductions): the rest of the block was filled
+ * earlier on the stream (dk_p2p_block) -- how the opt-in SpMV + partial-dot epilogue
+ * publishes the SpMV's p.q total with the following window's reductions. */
+int dk_launch_pub_ex(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+                     int64_t epoch, int point, int red_offset, int nred_total);
+/* device address of this rank's block for `point` in the board slot of `epoch`
+ * (nred_total doubles) */
+int dk_p2p_block(int64_t epoch, int point, int nred_total, uint64_t* ptr);
 /* stream-ordered wait until counts[q] points of every rank q have published
  * epoch `epoch` into this rank's board (flags consumed); a flag holding any
  * other epoch's tag is a protocol violation and traps; *gathered = the slot's

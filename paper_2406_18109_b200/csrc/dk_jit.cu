@@ -1997,31 +1997,54 @@ int dk_launch(int64_t handle, const dk_view* views, int nviews, const double* sc
   });
 }
 
+static void launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+                       int64_t epoch, int point, int red_offset, int nred_total) {
+  require_init();
+  require_not_capturing("dk_launch_pub (board slots are epoch-numbered)");
+  NvtxRange nv("dk_launch_pub", handle);
+  State& S = st();
+  if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
+  if (epoch < 0) fail(DK_ERR_ARG, "negative reduction epoch");
+  const int slot = (int)(epoch % DK_P2P_SLOTS);
+  if (point < 0 || point >= DK_P2P_POINTS) fail(DK_ERR_ARG, "point %d exceeds the board's %d points per rank", point, DK_P2P_POINTS);
+  KernelObj& k = kernel_of(handle);
+  const int nred = k.prog.nreduce;
+  if (nred_total <= 0) nred_total = nred;
+  if (nred == 0 || red_offset < 0 || red_offset + nred > nred_total || nred_total > DK_P2P_RED)
+    fail(DK_ERR_UNSUPPORTED, "kernel has %d reductions at %d of %d (board holds 1..%d)", nred, red_offset, nred_total,
+         DK_P2P_RED);
+  const size_t off = 8ull * (size_t)nred_total * (size_t)(S.rank * DK_P2P_POINTS + point);
+  DkPub pub = {};
+  pub.n = S.world;
+  pub.nred = nred_total;
+  pub.tag = p2p_tag(epoch);
+  pub.src = (uint64_t)S.board + p2p_data_off(slot) + off;
+  for (int q = 0; q < S.world; ++q) {
+    pub.dst[q] = S.peer_board[q] + p2p_data_off(slot) + off;
+    pub.flag[q] = S.peer_board[q] + p2p_flag_off(slot) + 4ull * (size_t)(S.rank * DK_P2P_POINTS + point);
+  }
+  launch(k, views, nviews, scalars, nscalars, pub.src + 8ull * (uint64_t)red_offset, &pub);
+}
+
 int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
                   int64_t epoch, int point) {
+  return guard([&] { launch_pub(handle, views, nviews, scalars, nscalars, epoch, point, 0, 0); });
+}
+
+int dk_launch_pub_ex(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
+                     int64_t epoch, int point, int red_offset, int nred_total) {
+  return guard([&] { launch_pub(handle, views, nviews, scalars, nscalars, epoch, point, red_offset, nred_total); });
+}
+
+int dk_p2p_block(int64_t epoch, int point, int nred_total, uint64_t* ptr) {
   return guard([&] {
     require_init();
-    require_not_capturing("dk_launch_pub (board slots are epoch-numbered)");
-    NvtxRange nv("dk_launch_pub", handle);
     State& S = st();
     if (!S.p2p) fail(DK_ERR_STATE, "dk_p2p_init has not enabled peer-memory reductions");
-    if (epoch < 0) fail(DK_ERR_ARG, "negative reduction epoch");
+    if (epoch < 0 || point < 0 || point >= DK_P2P_POINTS || nred_total <= 0 || nred_total > DK_P2P_RED)
+      fail(DK_ERR_ARG, "bad board block (epoch %lld, point %d, %d totals)", (long long)epoch, point, nred_total);
     const int slot = (int)(epoch % DK_P2P_SLOTS);
-    if (point < 0 || point >= DK_P2P_POINTS) fail(DK_ERR_ARG, "point %d exceeds the board's %d points per rank", point, DK_P2P_POINTS);
-    KernelObj& k = kernel_of(handle);
-    const int nred = k.prog.nreduce;
-    if (nred == 0 || nred > DK_P2P_RED) fail(DK_ERR_UNSUPPORTED, "kernel has %d reductions (board holds 1..%d)", nred, DK_P2P_RED);
-    const size_t off = 8ull * (size_t)nred * (size_t)(S.rank * DK_P2P_POINTS + point);
-    DkPub pub = {};
-    pub.n = S.world;
-    pub.nred = nred;
-    pub.tag = p2p_tag(epoch);
-    pub.src = (uint64_t)S.board + p2p_data_off(slot) + off;
-    for (int q = 0; q < S.world; ++q) {
-      pub.dst[q] = S.peer_board[q] + p2p_data_off(slot) + off;
-      pub.flag[q] = S.peer_board[q] + p2p_flag_off(slot) + 4ull * (size_t)(S.rank * DK_P2P_POINTS + point);
-    }
-    launch(k, views, nviews, scalars, nscalars, pub.src, &pub);
+    *ptr = (uint64_t)S.board + p2p_data_off(slot) + 8ull * (size_t)nred_total * (size_t)(S.rank * DK_P2P_POINTS + point);
   });
 }
 

@@ -140,7 +140,7 @@ class Executor:
         # opt-in SpMV + partial-dot epilogue (backend-only; the fusion plan is unchanged)
         if fuse_spmv_dot is None:
             fuse_spmv_dot = os.environ.get("DK_FUSE_SPMV_DOT", "0") == "1"
-        self.fuse_spmv_dot = bool(fuse_spmv_dot) and world == 1
+        self.fuse_spmv_dot = bool(fuse_spmv_dot)
         self._sd = None  # partials of the last SPMV_CSR, waiting for the window that reduces p.q
         self.spmv_dot_stats = {"spmv": 0, "consumed": 0}
 
@@ -992,17 +992,41 @@ class Executor:
             views[4] = self.view(r_y, ((y0 + a,), (y0 + b,)))
             return views
 
-        launches = [rows(a, b) for a, b in ((nx, t - nx), (0, nx), (t - nx, t)) if b > a]
+        spans = [(a, b) for a, b in ((nx, t - nx), (0, nx), (t - nx, t)) if b > a]
+        launches = [rows(a, b) for a, b in spans]
         sends = [(x[0], x[1], x[3]) for x in moves if x[2] == self.rank]
         recvs = [(x[0], x[1], x[2]) for x in moves if x[3] == self.rank]
+        dot = None
+        if self.fuse_spmv_dot and self.shape(task.args[3].store) == self.shape(task.args[4].store):
+            # the partial-dot epilogue per row span, partials contiguous in one buffer
+            parts = c_uint64()
+            check(self.lib.dk_scratch_alloc(8 * 4096 * len(spans), byref(parts)))
+            dot = (parts.value, [y0 + a for a, _b in spans])
+            if self._rec is not None:
+                self._rec["ok"] = False
         if self._rec is not None:
             slots = [(j, a.store) for j, a in enumerate(task.args)]
             self._rec["overlap"] = {"sends": sends, "recvs": recvs, "views": [(v, slots) for v in launches]}
-        self._issue_spmv_overlap(sends, recvs, launches)
+        nparts = self._issue_spmv_overlap(sends, recvs, launches, dot)
+        if dot is not None:
+            self._sd = {"x": task.args[3].store, "y": task.args[4].store, "pts": {i: (rects[i][4], dot[0], nparts)}}
+            self.spmv_dot_stats["spmv"] += 1
 
-    def _issue_spmv_overlap(self, sends, recvs, launches) -> None:
+    def _issue_spmv_overlap(self, sends, recvs, launches, dot=None) -> int:
         """Side stream: the halo sends (copy engine); main stream: the interior rows, the halo
-        receives, the boundary rows.  ``sends`` / ``recvs``: (store, rect, peer)."""
+        receives, the boundary rows.  ``sends`` / ``recvs``: (store, rect, peer).  ``dot``:
+        (partials buffer, first x row per launch) for the partial-dot epilogue; returns the
+        number of partials written."""
+        nparts = 0
+
+        def spmv(k, views):
+            nonlocal nparts
+            if dot is None:
+                check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
+                return
+            np_ = c_int()
+            check(self.lib.dk_spmv_csr_dot(views, dot[0] + 8 * nparts, dot[1][k], byref(np_)))
+            nparts += np_.value
 
         def enc(lst):
             m = len(lst)
@@ -1035,16 +1059,17 @@ class Executor:
             finally:
                 check(self.lib.dk_set_stream(main))
         wflags = (c_int32 * 5)(0, 0, 0, 0, 1)
-        check(self.lib.dk_builtin(b"SPMV_CSR", launches[0], 5, wflags))  # interior: own x rows only
+        spmv(0, launches[0])  # interior: own x rows only
         self.mark("interior_done")
         if recvs:
             check(self.lib.dk_dma_recv(*enc(recvs)))
         self.mark("halo_in")
-        for views in launches[1:]:
-            check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
+        for k, views in enumerate(launches[1:], 1):
+            spmv(k, views)
         if sends:
             check(self.lib.dk_stream_wait_event(self._side_ev[1]))  # p is not rewritten before the sends read it
         self.stats.p2p_halos += 1
+        return nparts
 
     def _csr_footprint(self, task: TaskDesc, p, full):
         """Columns of x an SPMV_CSR tile actually reads (NonePart reads the whole store).
@@ -1184,25 +1209,38 @@ class Executor:
                 f"task {task.kind} carries {len(task.scalars)} scalars, kernel expects {len(kp.scalar_names)}"
             )
         sd_fold = None
-        if spmv_dot is not None and self.world == 1:
+        sd_pub = None  # several GPUs: (position of p.q among the reductions, their count, original kernel)
+        if spmv_dot is not None:
             m = self._spmv_dot_match(task, kp, mine, rects, spmv_dot)
             if m is not None:
                 n, k, tslot = m
-                key = (id(kp), "spmv_dot", n, k)
-                hit = self._alias_k.get(key)
-                if hit is None or hit[0] is not kp:
-                    nests = list(kp.nests)
-                    dom, rank, stmts = nests[n]
-                    nests[n] = (dom, rank, stmts[:k] + stmts[k + 1:])
-                    hit = (kp, KProg(kp.slots, kp.scalar_names, kp.ntemps, tuple(nests), kp.fused_names))
-                    self._alias_k[key] = hit
-                sd_fold = (tslot, spmv_dot)
-                kp = hit[1]
+                order = [(n2, k2) for n2, (_d, _r, sts) in enumerate(kp.nests) for k2, st in enumerate(sts)
+                         if st[0] == "reduce"]
+                ridx = order.index((n, k))
+                # several GPUs: the SpMV's per-point p.q total rides in the window's own board block,
+                # which needs it first or last among the reductions (the kernel writes the rest)
+                ok = self.world == 1 or (self._p2p and not isolated and ridx in (0, len(order) - 1)
+                                         and len(order) <= runtime.P2P_RED)
+                if ok:
+                    key = (id(kp), "spmv_dot", n, k)
+                    hit = self._alias_k.get(key)
+                    if hit is None or hit[0] is not kp:
+                        nests = list(kp.nests)
+                        dom, rank, stmts = nests[n]
+                        nests[n] = (dom, rank, stmts[:k] + stmts[k + 1:])
+                        hit = (kp, KProg(kp.slots, kp.scalar_names, kp.ntemps, tuple(nests), kp.fused_names))
+                        self._alias_k[key] = hit
+                    if self.world == 1:
+                        sd_fold = (tslot, spmv_dot)
+                    else:
+                        sd_pub = (ridx, len(order), kp, spmv_dot)
+                    kp = hit[1]
         h, nred = self.kernel_handle(kp)
         scal = self._scalars(task.scalars)
         nslots = len(kp.slots)
+        red_kp = kp if sd_pub is None else sd_pub[2]
         red_targets = [
-            (st[1], kp.slots[st[1]]) for _, _, stmts in kp.nests for st in stmts if st[0] == "reduce"
+            (st[1], red_kp.slots[st[1]]) for _, _, stmts in red_kp.nests for st in stmts if st[0] == "reduce"
         ]
         use_totals = (self.world > 1 or isolated) and nred > 0
         V = len(prank)
@@ -1222,6 +1260,8 @@ class Executor:
                 pub_slot = self._p2p_epoch  # the reduction epoch (board slot = epoch mod P2P_SLOTS)
                 self._p2p_epoch += 1
                 use_totals = False
+        if sd_pub is not None and pub_slot < 0:
+            raise BackendError("SpMV + partial-dot epilogue without the peer-board reduction path")
         if use_totals:
             nbytes = 8 * maxp * nred
             tb = c_uint64()
@@ -1237,7 +1277,7 @@ class Executor:
                 self._rec["pub"] = True
                 self._rec["counts"] = (c_int32 * self.world)(*counts)
         aliased = self._alias_candidates(kp, task)
-        if sd_fold is not None:
+        if sd_fold is not None or sd_pub is not None:
             recorded = None
             if self._rec is not None:
                 self._rec["ok"] = False
@@ -1278,7 +1318,20 @@ class Executor:
                 views[si], p = self._copy_in(views[si])
                 scratch.append(p)
             hl = h if h_pt is None else h_pt
-            if pub_slot >= 0:
+            if sd_pub is not None:
+                # the point's p.q total (its SpMV partials folded in order) goes into its board
+                # block first; the window kernel writes its own totals beside it and publishes all
+                ridx, ntot, _kp0, sd = sd_pub
+                blk = c_uint64()
+                check(self.lib.dk_p2p_block(pub_slot, slot_in_rank, ntot, byref(blk)))
+                pv = dk_view()
+                pv.ptr, pv.rank, pv.dtype = blk.value + 8 * ridx, 0, DK_F64
+                _rect, parts, nparts = sd["pts"][i]
+                check(self.lib.dk_memset_zero(pv.ptr, 8))
+                check(self.lib.dk_accum(byref(pv), parts, 0, 1, nparts))
+                check(self.lib.dk_launch_pub_ex(hl, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank,
+                                                1 if ridx == 0 else 0, ntot))
+            elif pub_slot >= 0:
                 check(self.lib.dk_launch_pub(hl, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank))
             else:
                 tot = totals + 8 * nred * (self.rank * maxp + slot_in_rank) if use_totals else 0
@@ -1325,9 +1378,11 @@ class Executor:
             ops = []
             self._collect = ops
             try:
-                self._fold(task, kp, prank, rects, red_targets, 0, runtime.P2P_POINTS, nred)
+                self._fold(task, red_kp, prank, rects, red_targets, 0, runtime.P2P_POINTS, len(red_targets))
             finally:
                 self._collect = None
+            if sd_pub is not None:
+                self.spmv_dot_stats["consumed"] += 1
             self._p2p_fold(pub_slot, (c_int32 * self.world)(*counts), ops)
             self.mark("wait_done")
             self.stats.p2p_folds += 1

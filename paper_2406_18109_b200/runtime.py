@@ -108,6 +108,9 @@ _SIGS = {
     "dk_timestamp": (c_int, [c_uint64, c_int64]),
     "dk_launch_pub": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_int64, c_int]),
     "dk_p2p_wait": (c_int, [c_int64, POINTER(c_int32), POINTER(c_uint64)]),
+    "dk_launch_pub_ex": (c_int, [c_int64, POINTER(dk_view), c_int, POINTER(c_double), c_int, c_int64, c_int, c_int,
+                                 c_int]),
+    "dk_p2p_block": (c_int, [c_int64, c_int, c_int, POINTER(c_uint64)]),
     "dk_p2p_wait_fold": (
         c_int,
         [c_int64, POINTER(c_int32), c_int, POINTER(c_uint64), POINTER(c_int64), POINTER(c_int64), POINTER(c_int32)],

@@ -609,6 +609,27 @@ class FakeLib:
         self.p2p_nred[slot] = nred
         return self.dk_launch(h, views, nviews, scalars, nscal, self.board_ptr + off)
 
+    def dk_launch_pub_ex(self, h, views, nviews, scalars, nscal, epoch, point, red_offset, nred_total):
+        from paper_2406_18109_b200 import runtime as rt
+
+        slot = epoch % rt.P2P_SLOTS
+        nred = sum(1 for _, _, sts in self.kernels[h].nests for st in sts if st[0] == "reduce")
+        if nred_total <= 0:
+            nred_total = nred
+        assert 0 <= point < rt.P2P_POINTS and 0 < nred and 0 <= red_offset
+        assert red_offset + nred <= nred_total <= rt.P2P_RED
+        off = 8 * (slot * self.p2p_slot_doubles + nred_total * (self.rank * rt.P2P_POINTS + point) + red_offset)
+        self.p2p_nred[slot] = nred_total
+        return self.dk_launch(h, views, nviews, scalars, nscal, self.board_ptr + off)
+
+    def dk_p2p_block(self, epoch, point, nred_total, ref):
+        from paper_2406_18109_b200 import runtime as rt
+
+        assert epoch >= 0 and 0 <= point < rt.P2P_POINTS and 0 < nred_total <= rt.P2P_RED
+        slot = epoch % rt.P2P_SLOTS
+        _set(ref, self.board_ptr + 8 * (slot * self.p2p_slot_doubles + nred_total * (self.rank * rt.P2P_POINTS + point)))
+        return 0
+
     def dk_p2p_wait_fold(self, epoch, counts, nfold, targets, firsts, strides, ns):
         g = ctypes.c_uint64()
         rc = self.dk_p2p_wait(epoch, counts, ctypes.byref(g))

@@ -97,9 +97,30 @@ def main():
                 else:
                     bad.append((name, s))
     bad += gpusession_drop_in(rank, world, local)
+    consumed = 0
+    if os.environ.get("DK_P2P", "1") == "1":
+        # the SpMV + partial-dot epilogue across GPUs: p.q rides in the next window's board block
+        for name in ("cg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused", "pcg_csr_8x8_k2/fused"):
+            case = cases[name]
+            tr = PlanTrace.from_json(case["trace"])
+            ex = Executor(shapes=tr.shapes, seed=tr.seed, init=tr.init, dtypes=tr.dtypes, rank=rank, world=world,
+                          device=local, fuse_spmv_dot=True)
+            ex._comm = True
+            ex.enable_p2p()
+            replay(ex, tr.events)
+            got = {s: ex.get(s) for s in tr.live}
+            st = dict(ex.spmv_dot_stats)
+            ex.close()
+            consumed += st["consumed"]
+            if st["consumed"] < 3 or st["consumed"] != st["spmv"]:
+                bad.append((f"spmv_dot/{name}", str(st)))
+            if rank == 0:
+                for s, w in golden_arrays(case).items():
+                    if not np.allclose(got[s], w, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(w))))):
+                        bad.append((f"spmv_dot/{name}", s))
     if rank == 0:
         print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved} "
-              f"p2p_folds={p2p_folds} (DK_P2P={os.environ.get('DK_P2P', '1')})")
+              f"p2p_folds={p2p_folds} spmv_dot_consumed={consumed} (DK_P2P={os.environ.get('DK_P2P', '1')})")
         if bad:
             sys.exit(1)
     dist.barrier()

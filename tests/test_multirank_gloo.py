@@ -24,13 +24,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, names, q, p2p=False):
+def _worker(rank, world, port, names, q, p2p=False, fuse=False):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
     import torch.distributed as dist
 
     from fakedev import FakeLib
@@ -43,6 +44,7 @@ def _worker(rank, world, port, names, q, p2p=False):
     bad = []
     moved = 0
     hits = 0
+    fused = 0
     for name in names:
         if isinstance(name, dict):  # synthetic trace: compare with the oracle instead of a golden heap
             from oracle.interp import replay as oreplay
@@ -58,7 +60,7 @@ def _worker(rank, world, port, names, q, p2p=False):
             want_arrays = None
         lib = FakeLib(rank, world)
         ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, rank=rank,
-                      world=world, lib=lib)
+                      world=world, lib=lib, fuse_spmv_dot=fuse)
         ex._comm = True
         if p2p:
             lib.p2p_enabled = True
@@ -83,23 +85,30 @@ def _worker(rank, world, port, names, q, p2p=False):
             got = {s: ex.get(s) for s in trace.live}
             moved += (ex.stats.p2p_folds + ex.stats.p2p_halos) if p2p else ex.stats.transfers
             hits += ex.stats.mplan_hits
+            fused += ex.spmv_dot_stats["consumed"]
+            if fuse and ex.spmv_dot_stats["consumed"] != ex.spmv_dot_stats["spmv"]:
+                bad.append((name, f"spmv_dot {ex.spmv_dot_stats}"))
             if rank == 0:
                 want = want_arrays if want_arrays is not None else golden_arrays(case)
                 for s, w in want.items():
-                    if not same_bits(got[s], w):
+                    if fuse:  # p.q is summed in another order: rtol 1e-12
+                        tol = 1e-12 * max(1.0, float(np.max(np.abs(w)))) if np.size(w) else 0.0
+                        if not np.allclose(got[s], w, rtol=1e-12, atol=tol, equal_nan=True):
+                            bad.append((name, s))
+                    elif not same_bits(got[s], w):
                         bad.append((name, s))
         except Exception as e:  # noqa: BLE001
             bad.append((name, f"{type(e).__name__}: {e}"))
             break  # the peer may be blocked in a collective: stop instead of desynchronising
-    q.put((rank, bad, moved, hits))
+    q.put((rank, bad, moved, hits, fused))
     dist.destroy_process_group()
 
 
-def _run(names, world=2, p2p=False):
+def _run(names, world=2, p2p=False, fuse=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q, p2p)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, names, q, p2p, fuse)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]
@@ -215,6 +224,22 @@ def test_overlapped_halo_spmv_four_ranks():
     assert not bad, bad[:10]
     assert all(r[2] > 0 for r in res), res
     assert all(r[3] > 0 for r in res), res  # steady iterations replay the recorded overlap plan
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_spmv_dot_epilogue_across_ranks(world):
+    """DK_FUSE_SPMV_DOT on several GPUs: each rank's SpMV (plain, or the overlapped-halo split into
+    three row spans) emits p.q partials; the next window folds them into its own peer-board block
+    beside the totals it publishes, so the cross-rank fold is unchanged.  Heaps match the
+    reference within rtol 1e-12 (p.q is summed in another order)."""
+    if world == 2:
+        names = ["cg_csr_8x8_k2/fused", "pcg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused"]
+    else:
+        names = [t for t in _k8_traces() if "_k4/fused" in t["meta"]["name"]]
+    res = _run(names, world=world, p2p=True, fuse=True)
+    bad = [b for _, bs, *_ in res for b in bs]
+    assert not bad, bad[:10]
+    assert all(r[4] >= 3 for r in res), res
 
 
 def test_isolated_streams_two_ranks():
