@@ -146,9 +146,14 @@ int dk_builtin(const char* kind, const dk_view* views, int nviews, const int32_t
 /* SPMV_CSR with the opt-in partial-dot epilogue (DK_FUSE_SPMV_DOT=1; backend-only, it
  * changes which launch computes the following window's p.q, never the fusion plan):
  * views as dk_builtin("SPMV_CSR"); also writes per-CTA partials of sum_i x[x_row0+i]*y[i]
- * (i over this tile's rows, each partial a fixed in-order sum) to `parts` (device, room for
- * 4096 doubles) and their count to *nparts.  Replaces, for that window, the
- * DOT(p, q -> pq) reduction of the cg_like stream (trace.py:384-386). */
+ * (i over this tile's rows, each partial a fixed in-order sum) to parts[0 .. *nparts) and,
+ * from the last CTA, their fixed-order fold to parts[DK_SPMV_DOT_TOTAL].  `parts`: device,
+ * DK_SPMV_DOT_DOUBLES doubles; the 32-bit ticket at parts[DK_SPMV_DOT_PARTS] must be zero on
+ * entry (the kernel leaves it zero).  Replaces, for that window, the DOT(p, q -> pq)
+ * reduction of the cg_like stream (trace.py:384-386). */
+#define DK_SPMV_DOT_PARTS 4096
+#define DK_SPMV_DOT_TOTAL (DK_SPMV_DOT_PARTS + 1)
+#define DK_SPMV_DOT_DOUBLES (DK_SPMV_DOT_PARTS + 2)
 int dk_spmv_csr_dot(const dk_view* views, uint64_t parts, int64_t x_row0, int* nparts);
 
 /* multi-GPU (NCCL over NVLink/NVSwitch); one rank per process */

@@ -140,6 +140,7 @@ struct SpSharedT {
   SpStageT<R, CAP, S> st[S];
   unsigned long long full[S], empty[S];
   double red[R / 32];
+  int last;  // dot epilogue: this CTA folds the partials
 };
 __device__ __forceinline__ uint32_t sp_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -257,10 +258,30 @@ __global__ void __launch_bounds__(R + 32, MINB)
     for (int o = 16; o; o >>= 1) dacc = __dadd_rn(dacc, __shfl_xor_sync(0xffffffffu, dacc, o));
     if (lane == 0) SH.red[warp] = dacc;
     asm volatile("bar.sync 1, %0;" :: "r"(R) : "memory");  // consumers only
+    unsigned* ticket = reinterpret_cast<unsigned*>(dot + DK_SPMV_DOT_PARTS);
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < NC; ++w) t = __dadd_rn(t, SH.red[w]);
       dot[blockIdx.x] = t;
+      __threadfence();
+      SH.last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    asm volatile("bar.sync 1, %0;" :: "r"(R) : "memory");
+    if (SH.last) {
+      // the last CTA folds the per-CTA partials: strided in-order sums, then a fixed
+      // shuffle + warp-order tree (the grid depends only on nrows: run-to-run identical)
+      __threadfence();
+      double t = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += R) t = __dadd_rn(t, __ldcg(dot + i));
+      for (int o = 16; o; o >>= 1) t = __dadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+      if (lane == 0) SH.red[warp] = t;
+      asm volatile("bar.sync 1, %0;" :: "r"(R) : "memory");
+      if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < NC; ++w) u = __dadd_rn(u, SH.red[w]);
+        dot[DK_SPMV_DOT_TOTAL] = u;
+        *ticket = 0u;  // left zero for the buffer's next use
+      }
     }
   }
 }
@@ -414,7 +435,7 @@ int launch_spmv_csr_dot(const dk_view* v, double* parts, int64_t x_row0, cudaStr
   if (nrows == 0) return 0;
   const SpCfg& cfg = spmv_cfg();
   const int64_t nchunks = (nrows + cfg.rows - 1) / cfg.rows;
-  const int blocks = (int)std::min<int64_t>(std::min<int64_t>(nchunks, (int64_t)st().sm_count * cfg.minb), 4096);
+  const int blocks = (int)std::min<int64_t>(std::min<int64_t>(nchunks, (int64_t)st().sm_count * cfg.minb), DK_SPMV_DOT_PARTS);
   cfg.fn<<<blocks, cfg.threads, cfg.smem, s>>>((const int32_t*)rp.ptr, (const int32_t*)cl.ptr,
                                                (const double*)vl.ptr, (const double*)x.ptr, (double*)y.ptr, nrows,
                                                parts, x_row0);

@@ -141,7 +141,8 @@ class Executor:
         if fuse_spmv_dot is None:
             fuse_spmv_dot = os.environ.get("DK_FUSE_SPMV_DOT", "0") == "1"
         self.fuse_spmv_dot = bool(fuse_spmv_dot)
-        self._sd = None  # partials of the last SPMV_CSR, waiting for the window that reduces p.q
+        self._sd = None  # totals of the last SPMV_CSR's p.q, waiting for the window that reduces it
+        self._sd_buf = (0, 0)  # (device ptr, regions): dk_spmv_csr_dot partials + ticket + total
         self.spmv_dot_stats = {"spmv": 0, "consumed": 0}
 
     # ------------------------------------------------------------------ comm
@@ -205,10 +206,22 @@ class Executor:
         check(self.lib.dk_store_ensure(r.sid, lo, hi))
 
     def _drop_sd(self) -> None:
-        if self._sd is not None:
-            for _rect, ptr, _n in self._sd["pts"].values():
+        self._sd = None
+
+    def _sd_regions(self, n: int) -> int:
+        """Device buffer of ``n`` dk_spmv_csr_dot regions (SPMV_DOT_DOUBLES each, tickets zeroed
+        once; the kernel leaves them zero).  Kept across launches: a pending ``_sd`` is always
+        consumed or dropped before the next SpMV, and both are stream-ordered."""
+        ptr, have = self._sd_buf
+        if have < n:
+            if ptr:
                 check(self.lib.dk_scratch_free(ptr))
-            self._sd = None
+            have = max(4, n)
+            p = c_uint64()
+            check(self.lib.dk_scratch_alloc(8 * runtime.SPMV_DOT_DOUBLES * have, byref(p)))
+            check(self.lib.dk_memset_zero(p.value, 8 * runtime.SPMV_DOT_DOUBLES * have))
+            self._sd_buf = ptr, have = p.value, have
+        return ptr
 
     def free(self, sid: int) -> None:
         if self._sd is not None and sid in (self._sd["x"], self._sd["y"]):
@@ -222,6 +235,9 @@ class Executor:
         """Release every store this executor created (device state is process-global)."""
         self.drop_graphs()
         self._drop_sd()
+        if self._sd_buf[0]:
+            check(self.lib.dk_scratch_free(self._sd_buf[0]))
+            self._sd_buf = (0, 0)
         for sid in list(self.stores):
             self.free(sid)
         check(self.lib.dk_sync())
@@ -529,14 +545,10 @@ class Executor:
         temp_positions = frozenset(temp_positions)
         if self._sd is not None:
             sd, self._sd = self._sd, None
-            try:
-                if kp is not None and not isolated:
-                    self.drain()
-                    self._execute_planned(task, kp, temp_positions, None, spmv_dot=sd)
-                    return
-            finally:
-                for _rect, ptr, _n in sd["pts"].values():
-                    check(self.lib.dk_scratch_free(ptr))
+            if kp is not None and not isolated:
+                self.drain()
+                self._execute_planned(task, kp, temp_positions, None, spmv_dot=sd)
+                return
         if isolated:
             if kp is None:
                 raise BackendError(f"isolated execution needs a kernel for kind {task.kind!r}")
@@ -998,35 +1010,31 @@ class Executor:
         recvs = [(x[0], x[1], x[2]) for x in moves if x[3] == self.rank]
         dot = None
         if self.fuse_spmv_dot and self.shape(task.args[3].store) == self.shape(task.args[4].store):
-            # the partial-dot epilogue per row span, partials contiguous in one buffer
-            parts = c_uint64()
-            check(self.lib.dk_scratch_alloc(8 * 4096 * len(spans), byref(parts)))
-            dot = (parts.value, [y0 + a for a, _b in spans])
+            # the partial-dot epilogue per row span, one buffer region (and one total) per span
+            dot = (self._sd_regions(len(spans)), [y0 + a for a, _b in spans])
             if self._rec is not None:
                 self._rec["ok"] = False
         if self._rec is not None:
             slots = [(j, a.store) for j, a in enumerate(task.args)]
             self._rec["overlap"] = {"sends": sends, "recvs": recvs, "views": [(v, slots) for v in launches]}
-        nparts = self._issue_spmv_overlap(sends, recvs, launches, dot)
+        self._issue_spmv_overlap(sends, recvs, launches, dot)
         if dot is not None:
-            self._sd = {"x": task.args[3].store, "y": task.args[4].store, "pts": {i: (rects[i][4], dot[0], nparts)}}
+            D = runtime.SPMV_DOT_DOUBLES
+            self._sd = {"x": task.args[3].store, "y": task.args[4].store,
+                        "pts": {i: (rects[i][4], dot[0], runtime.SPMV_DOT_TOTAL, D, len(spans))}}
             self.spmv_dot_stats["spmv"] += 1
 
-    def _issue_spmv_overlap(self, sends, recvs, launches, dot=None) -> int:
+    def _issue_spmv_overlap(self, sends, recvs, launches, dot=None) -> None:
         """Side stream: the halo sends (copy engine); main stream: the interior rows, the halo
         receives, the boundary rows.  ``sends`` / ``recvs``: (store, rect, peer).  ``dot``:
-        (partials buffer, first x row per launch) for the partial-dot epilogue; returns the
-        number of partials written."""
-        nparts = 0
+        (dk_spmv_csr_dot regions, first x row per launch) for the partial-dot epilogue."""
 
         def spmv(k, views):
-            nonlocal nparts
             if dot is None:
                 check(self.lib.dk_builtin(b"SPMV_CSR", views, 5, wflags))
                 return
             np_ = c_int()
-            check(self.lib.dk_spmv_csr_dot(views, dot[0] + 8 * nparts, dot[1][k], byref(np_)))
-            nparts += np_.value
+            check(self.lib.dk_spmv_csr_dot(views, dot[0] + 8 * runtime.SPMV_DOT_DOUBLES * k, dot[1][k], byref(np_)))
 
         def enc(lst):
             m = len(lst)
@@ -1069,7 +1077,6 @@ class Executor:
         if sends:
             check(self.lib.dk_stream_wait_event(self._side_ev[1]))  # p is not rewritten before the sends read it
         self.stats.p2p_halos += 1
-        return nparts
 
     def _csr_footprint(self, task: TaskDesc, p, full):
         """Columns of x an SPMV_CSR tile actually reads (NonePart reads the whole store).
@@ -1326,9 +1333,9 @@ class Executor:
                 check(self.lib.dk_p2p_block(pub_slot, slot_in_rank, ntot, byref(blk)))
                 pv = dk_view()
                 pv.ptr, pv.rank, pv.dtype = blk.value + 8 * ridx, 0, DK_F64
-                _rect, parts, nparts = sd["pts"][i]
+                _rect, parts, first, stride, nt = sd["pts"][i]
                 check(self.lib.dk_memset_zero(pv.ptr, 8))
-                check(self.lib.dk_accum(byref(pv), parts, 0, 1, nparts))
+                check(self.lib.dk_accum(byref(pv), parts, first, stride, nt))
                 check(self.lib.dk_launch_pub_ex(hl, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank,
                                                 1 if ridx == 0 else 0, ntot))
             elif pub_slot >= 0:
@@ -1347,19 +1354,23 @@ class Executor:
             # the removed statement's p.q: each point's SpMV partials folded in a fixed order into
             # a total, then target += total in point order (executor.py:193-195)
             tslot, sd = sd_fold
-            tot = c_uint64()
-            check(self.lib.dk_scratch_alloc(8, byref(tot)))
-            tv0 = dk_view()
-            tv0.ptr, tv0.rank, tv0.dtype = tot.value, 0, DK_F64
             a = task.args[kp.slots[tslot].arg]
             r = self.stores[a.store]
             for i in sorted(mine):
-                _rect, parts, nparts = sd["pts"][i]
-                check(self.lib.dk_memset_zero(tot.value, 8))
-                check(self.lib.dk_accum(byref(tv0), parts, 0, 1, nparts))
+                _rect, parts, first, stride, nt = sd["pts"][i]
                 tv = self.view(r, rects[i][kp.slots[tslot].arg])
+                if nt == 1:
+                    check(self.lib.dk_accum(byref(tv), parts, first, stride, 1))
+                    continue
+                # several row spans: their totals folded first, then added (one total per point)
+                tot = c_uint64()
+                check(self.lib.dk_scratch_alloc(8, byref(tot)))
+                tv0 = dk_view()
+                tv0.ptr, tv0.rank, tv0.dtype = tot.value, 0, DK_F64
+                check(self.lib.dk_memset_zero(tot.value, 8))
+                check(self.lib.dk_accum(byref(tv0), parts, first, stride, nt))
                 check(self.lib.dk_accum(byref(tv), tot.value, 0, 1, 1))
-            check(self.lib.dk_scratch_free(tot.value))
+                check(self.lib.dk_scratch_free(tot.value))
             self.spmv_dot_stats["consumed"] += 1
         if use_totals:
             block = maxp * nred
@@ -1510,6 +1521,7 @@ class Executor:
             check(self.lib.dk_scratch_alloc(8 * block * (self.world + 1), byref(tb)))
             check(self.lib.dk_memset_zero(tb.value, 8 * block * (self.world + 1)))
         sd_pts = {}
+        sd_base = 0
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * max(n, 1))()
             for j, a in enumerate(task.args):
@@ -1536,12 +1548,14 @@ class Executor:
                 self._rec["ok"] = False
             if (self.fuse_spmv_dot and task.kind == "SPMV_CSR" and not scratch and not arenas
                     and len(rects[i][4][0]) == 1 and self.shape(task.args[3].store) == self.shape(task.args[4].store)):
-                # opt-in epilogue: the SpMV also emits partials of x_tile . y for the next window
-                parts = c_uint64()
-                check(self.lib.dk_scratch_alloc(8 * 4096, byref(parts)))
+                # opt-in epilogue: the SpMV also emits x_tile . y (per-CTA partials folded by its
+                # last CTA) for the next window; one buffer region per point
+                if not sd_base:
+                    sd_base = self._sd_regions(len(mine))
+                reg = sd_base + 8 * runtime.SPMV_DOT_DOUBLES * slot_in_rank
                 np_ = c_int()
-                check(self.lib.dk_spmv_csr_dot(views, parts.value, rects[i][4][0][0], byref(np_)))
-                sd_pts[i] = (rects[i][4], parts.value, np_.value)
+                check(self.lib.dk_spmv_csr_dot(views, reg, rects[i][4][0][0], byref(np_)))
+                sd_pts[i] = (rects[i][4], reg, runtime.SPMV_DOT_TOTAL, 1, 1)
                 if self._rec is not None:
                     self._rec["ok"] = False
             else:

@@ -129,6 +129,10 @@ P2P_POINTS = 16
 P2P_RED = 32
 P2P_MAIL_BYTES = 1 << 20
 P2P_FOLDS = 64
+# dk_spmv_csr_dot's partials buffer: per-CTA partials, the ticket word, the folded total
+SPMV_DOT_PARTS = 4096
+SPMV_DOT_TOTAL = SPMV_DOT_PARTS + 1
+SPMV_DOT_DOUBLES = SPMV_DOT_PARTS + 2
 
 EXPORTED = tuple(_SIGS)
 

@@ -399,8 +399,13 @@ class FakeLib:
         acc = 0.0
         for i in range(y.size):
             acc = acc + float(v[3].reshape(-1)[x_row0 + i]) * float(y[i])
+        from paper_2406_18109_b200 import runtime as rt
+
         pb, off = self._resolve(parts)
-        pb[off:].view(np.float64)[0] = acc
+        reg = pb[off:off + 8 * rt.SPMV_DOT_DOUBLES]
+        assert reg[8 * rt.SPMV_DOT_PARTS:8 * rt.SPMV_DOT_PARTS + 4].view(np.uint32)[0] == 0, "ticket not zero"
+        reg.view(np.float64)[0] = acc
+        reg.view(np.float64)[rt.SPMV_DOT_TOTAL] = 0.0 + acc
         _set(nparts_ref, 1)
         self.launches += 1
         return 0
