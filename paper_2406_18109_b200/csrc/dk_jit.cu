@@ -823,6 +823,30 @@ __device__ __forceinline__ double dk_warp_sum(double v) {
   return v;
 }
 
+// grid-wide barrier between the nests of a one-launch multi-nest window (cooperative
+// launch: every CTA is resident).  bar[0] arrivals, bar[1] generation.
+__device__ __forceinline__ void dk_grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x * gridDim.y - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(bar + 1), "r"(gen + 1u) : "memory");
+    } else {
+      unsigned g = gen;
+      while (g == gen) {
+        __nanosleep(64);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double dk_ldcg(const double* p) {
   double v;
   asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -852,6 +876,7 @@ struct GenOpts {
   int unroll = 2;
   int min_blocks = 4;
   bool stream_hint = false;  // evict-first (.cs) loads/stores for aligned streaming operands
+  bool merged = false;       // all nests in one cooperative launch, grid barriers between them
 };
 
 static GenOpts default_opts(const std::vector<NestPlan>& plans) {
@@ -897,12 +922,32 @@ class Gen {
   Gen(const Prog& g, const std::vector<NestPlan>& plans, const std::string& name = "dk", GenOpts opts = GenOpts(),
       std::vector<int> scalar_rep = {})
       : g_(g), plans_(plans), name_(name), kUnroll(opts.unroll), minb_(opts.min_blocks), cs_(opts.stream_hint),
-        opts_rep_(std::move(scalar_rep)) {}
+        merged_(opts.merged), opts_rep_(std::move(scalar_rep)) {}
 
   std::string source() {
     std::ostringstream o;
     o << kPrelude;
-    for (size_t n = 0; n < g_.nests.size(); ++n) nest(o, (int)n);
+    const int NN = (int)g_.nests.size();
+    for (int n = 0; n < NN; ++n) {
+      if (merged_) o << "#define threadIdx dk_tid\n#define blockDim dk_bdim\n";
+      nest(o, n);
+      if (merged_) o << "#undef threadIdx\n#undef blockDim\n";
+    }
+    if (merged_) {
+      // one launch for the whole window: each nest's body runs over the same
+      // 256-thread CTAs (its own TX x TY view of them), a grid barrier between nests
+      o << "\nstruct PM { uint64_t gbar; unsigned tx[" << (NN + 1) / 2 * 2 << "];";
+      for (int n = 0; n < NN; ++n) o << " P" << n << " p" << n << ";";
+      o << " };\n";
+      o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << minb_ << ") " << name_
+        << "_m(const __grid_constant__ PM P) {\n";
+      for (int n = 0; n < NN; ++n) {
+        if (n) o << "  dk_grid_sync((unsigned*)P.gbar);\n";
+        o << "  " << name_ << "_n" << n << "(P.p" << n << ", make_uint3(threadIdx.x % P.tx[" << n << "], threadIdx.x / P.tx["
+          << n << "], 0), dim3(P.tx[" << n << "], " << kTPB << " / P.tx[" << n << "], 1));\n";
+      }
+      o << "}\n";
+    }
     return o.str();
   }
 
@@ -913,6 +958,7 @@ class Gen {
   int kUnroll;
   int minb_;
   bool cs_;
+  bool merged_;
   std::vector<int> opts_rep_;
 
   int site_index(const NestPlan& np, int slot, const std::vector<int64_t>& offs) const {
@@ -1236,8 +1282,11 @@ class Gen {
     if (np.staged && !np.sweep) o << "alignas(64) unsigned char tm[128]; ";
     o << "DkHdr h; " << (NR ? "DkPub pub; " : "") << (np.sweep ? "DkUni u; " : "") << "DkSite s[" << std::max(NS, 1) << "]; dk_view rd[" << std::max(NR, 1)
       << "]; double sc[" << std::max(g_.nscal, 1) << "]; };\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << (np.st_ws ? kTPB + 32 : kTPB) << ", " << minb_ << ") " << name_ << "_n" << n
-      << "(const __grid_constant__ P" << n << " P) {\n";
+    if (merged_)
+      o << "static __device__ void " << name_ << "_n" << n << "(const P" << n << "& P, const uint3 dk_tid, const dim3 dk_bdim) {\n";
+    else
+      o << "extern \"C\" __global__ void __launch_bounds__(" << (np.st_ws ? kTPB + 32 : kTPB) << ", " << minb_ << ") " << name_ << "_n" << n
+        << "(const __grid_constant__ P" << n << " P) {\n";
     // hoisted rank-0 operands
     for (int i = 0; i < NS; ++i)
       if (np.sites[i].cls == 'S') o << "  const double S" << i << " = *(const double*)P.s[" << i << "].p;\n";
@@ -1612,6 +1661,8 @@ struct Module {
   std::vector<unsigned int*> ticket;
   std::string src;
   int unroll = 2;
+  bool merged = false;        // fn[0] runs every nest (cooperative launch, grid barriers)
+  unsigned int* gbar = nullptr;
   // red_part / ticket (and the K3 tile queue) are per-module scratch: two
   // launches of one module must not overlap.  Launches on one stream are
   // ordered; when a module moves to another stream the new stream first
@@ -1639,8 +1690,44 @@ struct Prepared {
   std::string sig;  // raw bytes of views + scalars + totals
   Module* m = nullptr;
   std::vector<std::vector<char>> blobs;
-  std::vector<unsigned> grid;  // gx, gy, tx, ty per nest
+  std::vector<unsigned> grid;  // gx, gy, tx, ty per nest (one entry for a merged module)
 };
+
+// a merged module's launch: cooperative (all CTAs resident for the grid barriers)
+static void launch_fn(CUfunction f, const unsigned* gd, void* blob, bool coop, CUstream s) {
+  void* args[] = {blob};
+  if (!coop) {
+    DK_CU(cuLaunchKernel(f, gd[0], gd[1], 1, gd[2], gd[3], 1, 0, s, args, nullptr));
+    return;
+  }
+  CUlaunchConfig cfg = {};
+  cfg.gridDimX = gd[0];
+  cfg.gridDimY = gd[1];
+  cfg.gridDimZ = 1;
+  cfg.blockDimX = gd[2];
+  cfg.blockDimY = gd[3];
+  cfg.blockDimZ = 1;
+  cfg.hStream = s;
+  CUlaunchAttribute at[1];
+  at[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+  at[0].value.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  DK_CU(cuLaunchKernelEx(&cfg, f, args, nullptr));
+}
+
+// one launch per window: every nest a plain streaming nest (or a rank-0 one), the
+// parameter block within the 32 KB kernel-parameter limit
+static bool mergeable(const Prog& g, const std::vector<NestPlan>& plans) {
+  if (plans.size() < 2 || getenv("DK_JIT_SPLIT_NESTS")) return false;
+  size_t bytes = 8 + 4 * (plans.size() + 1);
+  for (const NestPlan& np : plans) {
+    if (np.rank > 0 && (!np.oneshot || np.staged || np.sweep)) return false;
+    bytes += sizeof(DkHdr) + (np.red_slots.empty() ? 0 : sizeof(DkPub)) + 48 * std::max<size_t>(np.sites.size(), 1) +
+             sizeof(dk_view) * std::max<size_t>(np.red_slots.size(), 1) + 8 * std::max(g.nscal, 1);
+  }
+  return bytes <= 30000;
+}
 
 struct KernelObj {
   Prog prog;
@@ -1673,6 +1760,7 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
   char name[32];
   snprintf(name, sizeof name, "dkf_%08llx", (unsigned long long)(fnv1a(k.text) & 0xffffffffull));
   GenOpts opts = default_opts(plans);
+  opts.merged = m->merged = mergeable(k.prog, plans);
   std::vector<CUfunction> fns;
   for (;;) {
     Gen gen(k.prog, plans, name, opts, rep);
@@ -1683,9 +1771,9 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
     DK_CU(cuModuleLoadData(&m->mod, bin.data()));
     fns.clear();
     bool spills = false;
-    for (size_t n = 0; n < k.prog.nests.size(); ++n) {
+    for (size_t n = 0; n < (m->merged ? 1 : k.prog.nests.size()); ++n) {
       CUfunction f;
-      std::string nm = std::string(name) + "_n" + std::to_string(n);
+      std::string nm = std::string(name) + (m->merged ? std::string("_m") : "_n" + std::to_string(n));
       DK_CU(cuModuleGetFunction(&f, m->mod, nm.c_str()));
       int local = 0;
       DK_CU(cuFuncGetAttribute(&local, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f));
@@ -1699,12 +1787,16 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
   m->unroll = opts.unroll;
   g_jit_modules++;
   const int sms = st().sm_count;
+  if (m->merged) {
+    DK_CUDA(cudaMalloc(&m->gbar, sizeof(unsigned int) * 2));
+    DK_CUDA(cudaMemsetAsync(m->gbar, 0, sizeof(unsigned int) * 2, st().stream));
+  }
   for (size_t n = 0; n < k.prog.nests.size(); ++n) {
-    CUfunction f = fns[n];
+    CUfunction f = fns[m->merged ? 0 : n];
     int occ = 1;
     DK_CU(cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, plans[n].st_ws ? kTPB + 32 : kTPB, 0));
     occ = std::max(occ, 1);
-    m->fn.push_back(f);
+    if (!m->merged || n == 0) m->fn.push_back(f);
     m->occ.push_back(occ);
     double* rp = nullptr;
     unsigned int* tk = nullptr;
@@ -1758,9 +1850,7 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
     if (pr.sig != sig) continue;
     order_module(pr.m, S.stream);
     for (size_t n = 0; n < pr.blobs.size(); ++n) {
-      void* args[] = {pr.blobs[n].data()};
-      const unsigned* gd = &pr.grid[4 * n];
-      DK_CU(cuLaunchKernel(pr.m->fn[n], gd[0], gd[1], 1, gd[2], gd[3], 1, 0, (CUstream)S.stream, args, nullptr));
+      launch_fn(pr.m->fn[n], &pr.grid[4 * n], pr.blobs[n].data(), pr.m->merged, (CUstream)S.stream);
       S.launches++;
     }
     if (i) std::swap(k.recent[i], k.recent[0]);
@@ -1774,6 +1864,9 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
   order_module(m, S.stream);
   int kbase = 0;
   std::vector<char> blob;
+  std::vector<char> mblob;      // merged module: the nests' P_n blocks, in order
+  std::vector<unsigned> mtx;    // merged module: each nest's TX
+  int64_t mgx = 1;              // merged module: the largest per-nest grid
   for (size_t n = 0; n < g.nests.size(); ++n) {
     const NestPlan& np = fresh[n];
     const dk_view& dv = views[g.nests[n].dom];
@@ -1897,13 +1990,37 @@ static void launch(KernelObj& k, const dk_view* views, int nviews, const double*
       tx = np.st_ws ? kTPB + 32 : kTPB;
       ty = 1;
     }
-    // one by-value struct parameter; the driver copies sizeof(P_n) bytes from the blob
-    void* args[] = {blob.data()};
-    DK_CU(cuLaunchKernel(m->fn[n], gx, gy, 1, tx, ty, 1, 0, (CUstream)S.stream, args, nullptr));
-    S.launches++;
     kbase += NR;
+    if (m->merged) {
+      // the nest's P_n goes into the one PM block; its TX and grid are folded in below
+      blob.resize(total);
+      mblob.insert(mblob.end(), blob.begin(), blob.end());
+      mtx.push_back(r == 0 ? 32u : tx);
+      mgx = std::max<int64_t>(mgx, (int64_t)gx * gy);
+      continue;
+    }
+    // one by-value struct parameter; the driver copies sizeof(P_n) bytes from the blob
+    launch_fn(m->fn[n], std::vector<unsigned>{gx, gy, tx, ty}.data(), blob.data(), false, (CUstream)S.stream);
+    S.launches++;
     prep.blobs.push_back(blob);
     prep.grid.insert(prep.grid.end(), {gx, gy, tx, ty});
+  }
+  if (m->merged) {
+    // PM = { gbar, tx[NN rounded to even], P_0, P_1, ... }; every CTA resident (one wave)
+    const size_t NN = g.nests.size(), ntx = (NN + 1) / 2 * 2;
+    std::vector<char> pm(8 + 4 * ntx, 0);
+    const uint64_t gb = (uint64_t)m->gbar;
+    memcpy(pm.data(), &gb, 8);
+    memcpy(pm.data() + 8, mtx.data(), 4 * NN);
+    pm.insert(pm.end(), mblob.begin(), mblob.end());
+    pm.resize(pm.size() + 64, 0);
+    const int64_t wave = (int64_t)S.sm_count * m->occ[0];
+    const unsigned G = (unsigned)std::max<int64_t>(1, std::min<int64_t>(mgx, wave));
+    const unsigned gd[4] = {G, 1, (unsigned)kTPB, 1};
+    launch_fn(m->fn[0], gd, pm.data(), true, (CUstream)S.stream);
+    S.launches++;
+    prep.blobs.push_back(pm);
+    prep.grid.insert(prep.grid.end(), {gd[0], gd[1], gd[2], gd[3]});
   }
   if (k.recent.size() >= 8) k.recent.pop_back();
   k.recent.insert(k.recent.begin(), std::move(prep));
@@ -1959,7 +2076,9 @@ int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, in
           break;
         }
     }
-    Gen gen(g, plans, "dk", default_opts(plans), rep);
+    GenOpts opts = default_opts(plans);
+    opts.merged = mergeable(g, plans);
+    Gen gen(g, plans, "dk", opts, rep);
     std::string src = gen.source();
     if (compile) {
       std::string log;

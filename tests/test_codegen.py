@@ -171,3 +171,36 @@ def _copy_task(rank):
     ident = tuple(tuple(1 if i == j else 0 for j in range(rank)) for i in range(rank))
     p = PartDesc("tiling", (6,) * rank, (0,) * rank, ident, (0,) * rank)
     return TaskDesc("COPY", (1,) * rank, (ArgDesc(0, p, "R"), ArgDesc(1, p, "W")))
+
+
+def test_multi_nest_windows_compile_as_one_kernel(rt):
+    """Windows whose tasks iterate differently-shaped domains lower to several nests; every such
+    kernel of the fuzz corpus is generated as ONE cooperative kernel (``_m``: each nest a device
+    function over the same 256-thread CTAs, ``dk_grid_sync`` between nests) and compiles for sm_100a;
+    DK_JIT_SPLIT_NESTS=1 restores one launch per nest."""
+    import os
+
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    seen = set()
+    merged = 0
+    for case in load_golden("fuzz250.json.gz")[::3]:
+        tr = PlanTrace.from_json(case["trace"])
+        for e in tr.execs():
+            if e.kernel is None or len(e.kernel.nests) < 2:
+                continue
+            w = e.kernel.wire([s.decl_rank for s in e.kernel.slots])
+            if w in seen:
+                continue
+            seen.add(w)
+            src = codegen(rt, e.kernel, views_for(rt, e.task, e.kernel, tr.shapes), compile_=len(seen) <= 12)
+            assert src.count("__global__") == 1 and "dk_m(" in src, src[-2000:]
+            assert src.count("dk_grid_sync((unsigned*)P.gbar)") == len(e.kernel.nests) - 1
+            merged += 1
+    assert merged >= 20
+    os.environ["DK_JIT_SPLIT_NESTS"] = "1"
+    try:
+        src = codegen(rt, e.kernel, views_for(rt, e.task, e.kernel, tr.shapes), compile_=False)
+    finally:
+        del os.environ["DK_JIT_SPLIT_NESTS"]
+    assert src.count("__global__") == len(e.kernel.nests)

@@ -49,3 +49,46 @@ def test_graph_replay_of_last_iteration_matches_oracle(name):
             assert np.array_equal(got, want), f"store {sid} differs after graph replay"
     finally:
         ex.close()
+
+
+@pytest.mark.gpu
+def test_graph_capture_of_cooperative_multi_nest_window():
+    """A multi-nest window (one cooperative launch with grid barriers) captured into a CUDA graph
+    and relaunched leaves the same bytes as launching it directly a second time."""
+    from paper_2406_18109_b200.executor import Executor, replay
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    with gzip.open(os.path.join(REPO, "tests", "golden", "fuzz250.json.gz"), "rt") as f:
+        cases = json.load(f)["cases"]
+    done = 0
+    for case in cases:
+        trace = PlanTrace.from_json(case["trace"])
+        ev = trace.events
+        k = next((i for i, (kind, e) in enumerate(ev) if kind == "exec" and e.kernel is not None
+                  and len(e.kernel.nests) > 1), None)
+        if k is None:
+            continue
+        e = ev[k][1]
+        outs = []
+        for use_graph in (True, False):
+            ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, device=0)
+            try:
+                replay(ex, ev[:k + 1])
+                ex.sync()
+                if use_graph:
+                    g = ex.capture(lambda: ex.execute(e.task, e.kernel, e.temp_positions))
+                    ex.graph_launch(g)
+                    ex.sync()
+                    ex.graph_destroy(g)
+                else:
+                    ex.execute(e.task, e.kernel, e.temp_positions)
+                outs.append({a.store: ex.get(a.store) for j, a in enumerate(e.task.args)
+                             if j not in e.temp_positions and a.store in ex.stores})
+            finally:
+                ex.close()
+        for sid, want in outs[1].items():
+            assert np.array_equal(outs[0][sid], want, equal_nan=True), (case["name"], sid)
+        done += 1
+        if done == 5:
+            break
+    assert done == 5

@@ -91,6 +91,60 @@ def test_golden_bench_cases(Executor, bench_cases):
     assert exact_cases >= 5
 
 
+def test_multi_nest_windows_run_as_one_launch(Executor, fuzz_cases, monkeypatch):
+    """Fuzz windows with several nests run as ONE cooperative kernel per point (grid barriers
+    between the nests): the reference's bytes either way, and DK_JIT_SPLIT_NESTS=1 (one launch
+    per nest) costs exactly the extra nests' launches."""
+    from ctypes import byref, c_int64
+
+    from paper_2406_18109_b200.plan import PlanTrace
+
+    def launches(ex):
+        c = c_int64()
+        ex.lib.dk_launch_count(byref(c))
+        return c.value
+
+    def run(trace):
+        from paper_2406_18109_b200.executor import replay
+
+        ex = Executor(shapes=trace.shapes, seed=trace.seed, init=trace.init, dtypes=trace.dtypes, device=0)
+        try:
+            l0 = launches(ex)
+            replay(ex, trace.events)
+            ex.sync()
+            n = launches(ex) - l0
+            return {s: ex.get(s) for s in trace.live}, n
+        finally:
+            ex.close()
+
+    saved = expect = ncases = 0
+    for case in fuzz_cases:
+        trace = PlanTrace.from_json(case["trace"])
+        extra = 0
+        for e in trace.execs():
+            if e.kernel is not None and len(e.kernel.nests) > 1:
+                pts = 1
+                for d in e.task.launch:
+                    pts *= d
+                extra += (len(e.kernel.nests) - 1) * pts
+        if not extra:
+            continue
+        want = golden_arrays(case)
+        got, lm = run(trace)
+        _compare(case["name"], got, want, _integer_valued(want), trace)
+        monkeypatch.setenv("DK_JIT_SPLIT_NESTS", "1")
+        got, ls = run(trace)
+        monkeypatch.delenv("DK_JIT_SPLIT_NESTS")
+        _compare(case["name"] + "/split", got, want, _integer_valued(want), trace)
+        assert ls >= lm
+        saved += ls - lm
+        expect += extra
+        ncases += 1
+        if ncases == 30:
+            break
+    assert ncases >= 10 and saved == expect, (ncases, saved, expect)
+
+
 def test_golden_fuzz_corpus(Executor, fuzz_cases):
     from paper_2406_18109_b200.plan import PlanTrace
 
