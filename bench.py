@@ -691,7 +691,7 @@ def e2e_bs(ex, trace, steps, torch, ext_stream, world):
     by[:] = rng.integers(1, 10, size=n)
     from paper_2406_18109_b200.streaming import HostStreamer
 
-    streamer = HostStreamer(ex, chunks=16) if len(execs) == 1 else None
+    streamer = HostStreamer(ex, chunks=64) if len(execs) == 1 else None
     barrier(torch, world)
     ex.sync()
     start = torch.cuda.Event(enable_timing=True)
@@ -804,7 +804,7 @@ def run_gpusession(steps, rank, world, local, size=1_000_000_000, graphs=True, e
             out["streamed_windows"] = s.streamed_windows - streamed0
             out["path"] = ("GpuSession (drop-in): heap.arrays[x], heap.arrays[y] = pinned host arrays; "
                            "submit/flush the 67-task iteration -- the window reading them runs host-streamed "
-                           "(H2D / kernel / D2H of stream_out(out) in 16 chunks over 3 streams); "
+                           "(H2D / kernel / D2H of stream_out(out) in 64 chunks over 3 streams); "
                            "heap.get(out, out=pinned)")
         out["note"] = ("wall clock: reference front end (window analysis, memo replay, report) + GpuSession "
                        "execution")
@@ -960,7 +960,7 @@ def run_ours(args):
         e_ms, bi, bo, ok = main["e2e"]
         out["e2e"] = {"value": round(world * K / (e_ms / 1e3), 4), "unit": "iter/s", "h2d_bytes_per_step": bi,
                       "d2h_bytes_per_step": bo,
-                      "path": "streaming.HostStreamer: pinned H2D(x, y) / fused kernel / D2H(out) in 16 chunks over 3 streams",
+                      "path": "streaming.HostStreamer: pinned H2D(x, y) / fused kernel / D2H(out) in 64 chunks over 3 streams",
                       "result_check": "out == x + y (the chain's operator cycle is the identity)" if ok else "FAILED"}
     def spmv_dot_line(w2):
         # opt-in SpMV + partial-dot epilogue (BASELINE configs[3] "fused SpMV+dot+axpy"): same plan,

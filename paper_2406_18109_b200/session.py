@@ -193,7 +193,7 @@ class GpuSession(_RefSession):
         from .streaming import HostStreamer
 
         if self._streamer is None:
-            self._streamer = HostStreamer(self.executor, chunks=16)
+            self._streamer = HostStreamer(self.executor, chunks=64)
         outs = {sid: self._host_out[sid] for sid in writes if sid in self._host_out}
         try:
             self._streamer.run(task, kp, temp_positions, {sid: self._host_in[sid] for sid in ins}, outs)

@@ -22,6 +22,8 @@ from ctypes import byref, c_uint64
 import numpy as np
 
 from .errors import UnsupportedError
+import os
+
 from .ir import KProg, TaskDesc, rect_of
 from .runtime import check, dk_view
 
@@ -29,7 +31,7 @@ from .runtime import check, dk_view
 class HostStreamer:
     def __init__(self, ex, chunks: int = 8) -> None:
         self.ex = ex
-        self.chunks = max(1, chunks)
+        self.chunks = max(1, int(os.environ.get("DK_STREAM_CHUNKS", chunks)))
         lib = ex.lib
         self.main = ex.stream()
         self.streams = []
