@@ -981,7 +981,8 @@ def run_ours(args):
         try:
             un = one(wl, "unfused")
             out["unfused"] = {"value": round(world * K / (un["ms"] / 1e3), 4), "ms_per_step": round(un["ms"] / K, 3),
-                              "gpu_launches": un["launches"], "result_check": un["check"]}
+                              "gpu_launches": un["launches"], "result_check": un["check"],
+                              "per_exec_ms": un["dom"]["per_exec_ms"] if un["dom"] else None}
             out["fused_over_unfused"] = round(un["ms"] / main["ms"], 3)
         except Exception as exc:  # noqa: BLE001
             out["unfused"] = {"error": f"{type(exc).__name__}: {exc}"}
