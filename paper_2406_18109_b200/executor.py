@@ -143,7 +143,7 @@ class Executor:
         self.fuse_spmv_dot = bool(fuse_spmv_dot)
         self._sd = None  # totals of the last SPMV_CSR's p.q, waiting for the window that reduces it
         self._sd_buf = (0, 0)  # (device ptr, regions): dk_spmv_csr_dot partials + ticket + total
-        self.spmv_dot_stats = {"spmv": 0, "consumed": 0}
+        self.spmv_dot_stats = {"spmv": 0, "consumed": 0, "replayed": 0}  # replayed: consumers from the plan cache
 
     # ------------------------------------------------------------------ comm
     def init_comm(self, unique_id: bytes) -> None:
@@ -543,9 +543,13 @@ class Executor:
         if kp is None and task.kind not in BUILTIN_KINDS:
             raise UnknownTaskKind(f"no generator or builtin for task kind {task.kind!r}")
         temp_positions = frozenset(temp_positions)
+        use_mplan = os.environ.get("DK_MPLAN", "1") != "0"
+        sd = None
         if self._sd is not None:
             sd, self._sd = self._sd, None
-            if kp is not None and not isolated:
+            if kp is None or isolated:
+                sd = None
+            elif self.world == 1 or not use_mplan:
                 self.drain()
                 self._execute_planned(task, kp, temp_positions, None, spmv_dot=sd)
                 return
@@ -556,7 +560,6 @@ class Executor:
             self.check_isolated(task, temp_positions)
             self._execute_planned(task, kp, temp_positions, None, isolated=True)
             return
-        use_mplan = os.environ.get("DK_MPLAN", "1") != "0"
         pkey = None
         if kp is not None and self.world == 1:
             # key on the non-temporary arguments: each memo replay of a window names fresh
@@ -580,14 +583,20 @@ class Executor:
         self.drain()
         if use_mplan:
             key, sids = self._mplan_key(task, kp, temp_positions)
+            if key is not None and sd is not None:
+                # a window consuming the SpMV epilogue's p.q is its own plan
+                if sd["x"] not in sids or sd["y"] not in sids:
+                    key = None
+                else:
+                    key = key + (("spmv_dot", sids.index(sd["x"]), sids.index(sd["y"]), tuple(sorted(sd["pts"]))),)
             hit = self._mplans.get(key) if key is not None else None
             if hit is not None and hit["kp"] is kp:
-                self._mplan_replay(hit, task, kp, sids)
+                self._mplan_replay(hit, task, kp, sids, sd)
                 return
             self._rec = {"ok": key is not None, "xfer": None, "views": [], "fold": [], "pub": False,
                          "ensure": [], "inits": []}
             try:
-                self._execute_planned(task, kp, temp_positions, pkey)
+                self._execute_planned(task, kp, temp_positions, pkey, spmv_dot=sd)
                 if self._rec["ok"]:
                     self._mplan_store(key, sids, kp)
             finally:
@@ -737,6 +746,13 @@ class Executor:
                 return
             plan["overlap"] = {"sends": [(cidx[sid], r, q) for sid, r, q in ov["sends"]],
                                "recvs": [(cidx[sid], r, q) for sid, r, q in ov["recvs"]], "views": cvs}
+            d = ov.get("dot")
+            if d is not None:
+                if d["x"] not in cidx or d["y"] not in cidx:
+                    return
+                plan["overlap"]["dot"] = dict(d, x=cidx[d["x"]], y=cidx[d["y"]])
+        if rec.get("sdpub") is not None:
+            plan["sdpub"] = rec["sdpub"]
         plan["views"], plan["fold"] = vs, fold
         dev = set()
         for item in vs:
@@ -776,7 +792,7 @@ class Executor:
             nv[idx].ptr = bases[c] + off
         return nv
 
-    def _mplan_replay(self, hit, task, kp, sids) -> None:
+    def _mplan_replay(self, hit, task, kp, sids, sd=None) -> None:
         recs = [self.rec(sid) for sid in sids]
         for c, rects in hit["inits"]:
             self._materialize_init(recs[c], rects)
@@ -793,10 +809,17 @@ class Executor:
             self.stats.bytes_moved += nbytes
         if kp is None and hit.get("overlap") is not None:
             ov = hit["overlap"]
+            d = ov.get("dot")
+            dot = None if d is None else (self._sd_regions(len(d["rows"])), d["rows"])
             self._issue_spmv_overlap([(sids[c], r, q) for c, r, q in ov["sends"]],
                                      [(sids[c], r, q) for c, r, q in ov["recvs"]],
-                                     [self._rebind(cv, bases) for cv in ov["views"]])
+                                     [self._rebind(cv, bases) for cv in ov["views"]], dot)
             self.stats.bytes_moved += sum(rg.volume(r) * recs[c].esize for c, r, _q in ov["recvs"] + ov["sends"])
+            if d is not None:
+                self._sd = {"x": sids[d["x"]], "y": sids[d["y"]],
+                            "pts": {d["i"]: (d["yrect"], dot[0], runtime.SPMV_DOT_TOTAL, runtime.SPMV_DOT_DOUBLES,
+                                             len(d["rows"]))}}
+                self.spmv_dot_stats["spmv"] += 1
         elif kp is None:
             kind = task.kind.encode()
             for cv, n, wflags in hit["views"]:
@@ -805,7 +828,23 @@ class Executor:
             h, _ = self.kernel_handle(kp)
             scal = self._scalars(task.scalars)
             ns, nsl = len(task.scalars), len(kp.slots)
-            if hit["pub"]:
+            sp = hit.get("sdpub")
+            if hit["pub"] and sp is not None:
+                # the recorded window consumed the SpMV epilogue's p.q (Executor._run_kernel)
+                epoch = self._p2p_epoch
+                self._p2p_epoch += 1
+                for sir, cv in enumerate(hit["views"]):
+                    self._sd_publish(epoch, sir, sp["ridx"], sp["ntot"], sd["pts"][sp["pts"][sir]])
+                    check(self.lib.dk_launch_pub_ex(sp["h"], self._rebind(cv, bases), nsl, scal, ns, epoch, sir,
+                                                    1 if sp["ridx"] == 0 else 0, sp["ntot"]))
+                self.spmv_dot_stats["consumed"] += 1
+                self.spmv_dot_stats["replayed"] += 1
+                self.mark("pub_done")
+                self._p2p_fold(epoch, hit["counts"], [(self._rebind(cv, bases), first, stride, nv)
+                                                      for cv, first, stride, nv in hit["fold"]])
+                self.mark("wait_done")
+                self.stats.p2p_folds += 1
+            elif hit["pub"]:
                 epoch = self._p2p_epoch
                 self._p2p_epoch += 1
                 for sir, cv in enumerate(hit["views"]):
@@ -1012,11 +1051,12 @@ class Executor:
         if self.fuse_spmv_dot and self.shape(task.args[3].store) == self.shape(task.args[4].store):
             # the partial-dot epilogue per row span, one buffer region (and one total) per span
             dot = (self._sd_regions(len(spans)), [y0 + a for a, _b in spans])
-            if self._rec is not None:
-                self._rec["ok"] = False
         if self._rec is not None:
             slots = [(j, a.store) for j, a in enumerate(task.args)]
             self._rec["overlap"] = {"sends": sends, "recvs": recvs, "views": [(v, slots) for v in launches]}
+            if dot is not None:
+                self._rec["overlap"]["dot"] = {"rows": dot[1], "i": i, "yrect": rects[i][4],
+                                               "x": task.args[3].store, "y": task.args[4].store}
         self._issue_spmv_overlap(sends, recvs, launches, dot)
         if dot is not None:
             D = runtime.SPMV_DOT_DOUBLES
@@ -1226,8 +1266,12 @@ class Executor:
                 ridx = order.index((n, k))
                 # several GPUs: the SpMV's per-point p.q total rides in the window's own board block,
                 # which needs it first or last among the reductions (the kernel writes the rest)
+                cnt = [0] * self.world
+                for q in prank:
+                    cnt[q] += 1
                 ok = self.world == 1 or (self._p2p and not isolated and ridx in (0, len(order) - 1)
-                                         and len(order) <= runtime.P2P_RED)
+                                         and len(order) <= runtime.P2P_RED and min(cnt) >= 1
+                                         and max(cnt) <= runtime.P2P_POINTS)
                 if ok:
                     key = (id(kp), "spmv_dot", n, k)
                     hit = self._alias_k.get(key)
@@ -1287,7 +1331,10 @@ class Executor:
         if sd_fold is not None or sd_pub is not None:
             recorded = None
             if self._rec is not None:
-                self._rec["ok"] = False
+                if sd_pub is not None and pub_slot >= 0 and not aliased:
+                    self._rec["sdpub"] = {"ridx": sd_pub[0], "ntot": sd_pub[1], "h": h, "pts": list(mine)}
+                else:
+                    self._rec["ok"] = False
         if aliased:
             recorded = None  # copy-ins and rewritten kernels are planned per launch
             if self._rec is not None:
@@ -1329,13 +1376,7 @@ class Executor:
                 # the point's p.q total (its SpMV partials folded in order) goes into its board
                 # block first; the window kernel writes its own totals beside it and publishes all
                 ridx, ntot, _kp0, sd = sd_pub
-                blk = c_uint64()
-                check(self.lib.dk_p2p_block(pub_slot, slot_in_rank, ntot, byref(blk)))
-                pv = dk_view()
-                pv.ptr, pv.rank, pv.dtype = blk.value + 8 * ridx, 0, DK_F64
-                _rect, parts, first, stride, nt = sd["pts"][i]
-                check(self.lib.dk_memset_zero(pv.ptr, 8))
-                check(self.lib.dk_accum(byref(pv), parts, first, stride, nt))
+                self._sd_publish(pub_slot, slot_in_rank, ridx, ntot, sd["pts"][i])
                 check(self.lib.dk_launch_pub_ex(hl, views, nslots, scal, len(task.scalars), pub_slot, slot_in_rank,
                                                 1 if ridx == 0 else 0, ntot))
             elif pub_slot >= 0:
@@ -1398,6 +1439,17 @@ class Executor:
             self.mark("wait_done")
             self.stats.p2p_folds += 1
         return recorded
+
+    def _sd_publish(self, epoch, point, ridx, ntot, pt) -> None:
+        """The point's p.q total (its SpMV row spans' totals folded in order) into its board
+        block at statement position ``ridx``, before the window kernel publishes the block."""
+        _rect, parts, first, stride, nt = pt
+        blk = c_uint64()
+        check(self.lib.dk_p2p_block(epoch, point, ntot, byref(blk)))
+        pv = dk_view()
+        pv.ptr, pv.rank, pv.dtype = blk.value + 8 * ridx, 0, DK_F64
+        check(self.lib.dk_memset_zero(pv.ptr, 8))
+        check(self.lib.dk_accum(byref(pv), parts, first, stride, nt))
 
     def _accum(self, sid, tv, gathered, first, stride, n) -> None:
         if self._collect is not None:
@@ -1522,6 +1574,9 @@ class Executor:
             check(self.lib.dk_memset_zero(tb.value, 8 * block * (self.world + 1)))
         sd_pts = {}
         sd_base = 0
+        # several GPUs: the consuming window can only carry p.q through its peer-board block
+        # when every rank owns a point (Executor._run_kernel)
+        sd_ok = self.world == 1 or (self._p2p and len(set(prank)) == self.world)
         for slot_in_rank, i in enumerate(mine):
             views = (dk_view * max(n, 1))()
             for j, a in enumerate(task.args):
@@ -1546,7 +1601,7 @@ class Executor:
                     scratch.append(p)
             if scratch and self._rec is not None:
                 self._rec["ok"] = False
-            if (self.fuse_spmv_dot and task.kind == "SPMV_CSR" and not scratch and not arenas
+            if (self.fuse_spmv_dot and task.kind == "SPMV_CSR" and not scratch and not arenas and sd_ok
                     and len(rects[i][4][0]) == 1 and self.shape(task.args[3].store) == self.shape(task.args[4].store)):
                 # opt-in epilogue: the SpMV also emits x_tile . y (per-CTA partials folded by its
                 # last CTA) for the next window; one buffer region per point

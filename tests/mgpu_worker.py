@@ -112,12 +112,16 @@ def main():
             st = dict(ex.spmv_dot_stats)
             ex.close()
             consumed += st["consumed"]
-            if st["consumed"] < 3 or st["consumed"] != st["spmv"]:
+            # every rank must own a point of the SpMV for the epilogue to be used across GPUs
+            spmv_vol = max(e.task.volume for e in tr.execs() if e.task.kind == "SPMV_CSR")
+            if st["consumed"] != st["spmv"] or (spmv_vol >= world and st["consumed"] < 3):
                 bad.append((f"spmv_dot/{name}", str(st)))
             if rank == 0:
                 for s, w in golden_arrays(case).items():
                     if not np.allclose(got[s], w, rtol=1e-12, atol=1e-12 * max(1.0, float(np.max(np.abs(w))))):
                         bad.append((f"spmv_dot/{name}", s))
+    if os.environ.get("DK_P2P", "1") == "1" and consumed == 0:
+        bad.append(("spmv_dot", "never used"))
     if rank == 0:
         print(f"MGPU world={world} cases={len(names)} stores exact={exact} within_rtol={close} bad={bad[:8]} transfers={moved} "
               f"p2p_folds={p2p_folds} spmv_dot_consumed={consumed} (DK_P2P={os.environ.get('DK_P2P', '1')})")

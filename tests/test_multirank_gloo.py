@@ -45,6 +45,7 @@ def _worker(rank, world, port, names, q, p2p=False, fuse=False):
     moved = 0
     hits = 0
     fused = 0
+    replayed = 0
     for name in names:
         if isinstance(name, dict):  # synthetic trace: compare with the oracle instead of a golden heap
             from oracle.interp import replay as oreplay
@@ -86,6 +87,7 @@ def _worker(rank, world, port, names, q, p2p=False, fuse=False):
             moved += (ex.stats.p2p_folds + ex.stats.p2p_halos) if p2p else ex.stats.transfers
             hits += ex.stats.mplan_hits
             fused += ex.spmv_dot_stats["consumed"]
+            replayed += ex.spmv_dot_stats["replayed"]
             if fuse and ex.spmv_dot_stats["consumed"] != ex.spmv_dot_stats["spmv"]:
                 bad.append((name, f"spmv_dot {ex.spmv_dot_stats}"))
             if rank == 0:
@@ -100,7 +102,7 @@ def _worker(rank, world, port, names, q, p2p=False, fuse=False):
         except Exception as e:  # noqa: BLE001
             bad.append((name, f"{type(e).__name__}: {e}"))
             break  # the peer may be blocked in a collective: stop instead of desynchronising
-    q.put((rank, bad, moved, hits, fused))
+    q.put((rank, bad, moved, hits, fused, replayed))
     dist.destroy_process_group()
 
 
@@ -235,11 +237,14 @@ def test_spmv_dot_epilogue_across_ranks(world):
     if world == 2:
         names = ["cg_csr_8x8_k2/fused", "pcg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused"]
     else:
-        names = [t for t in _k8_traces() if "_k4/fused" in t["meta"]["name"]]
+        # + a 2-point plan on 4 ranks: two ranks own no point, so the epilogue must stay off
+        names = [t for t in _k8_traces() if "_k4/fused" in t["meta"]["name"]] + ["cg_csr_8x8_k2/fused"]
     res = _run(names, world=world, p2p=True, fuse=True)
     bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
     assert all(r[4] >= 3 for r in res), res
+    if world == 4:  # steady iterations (SpMV with the epilogue and its consumer) replayed from the plan cache
+        assert all(r[5] > 0 for r in res), res
 
 
 def test_isolated_streams_two_ranks():
