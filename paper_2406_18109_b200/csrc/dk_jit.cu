@@ -1717,11 +1717,23 @@ static void launch_fn(CUfunction f, const unsigned* gd, void* blob, bool coop, C
 }
 
 // one launch per window: every nest a plain streaming nest (or a rank-0 one), the
-// parameter block within the 32 KB kernel-parameter limit
-static bool mergeable(const Prog& g, const std::vector<NestPlan>& plans) {
+// parameter block within the 32 KB kernel-parameter limit, and every nest small
+// enough (DK_JIT_MERGE_MAX elements, default 2^21) that the launch it saves
+// matters more than the one-wave grid-stride walk the grid barrier requires (a
+// 32766^2 COPY: 3.24 ms grid-stride vs 2.48 ms one CTA per chunk)
+static bool mergeable(const Prog& g, const std::vector<NestPlan>& plans, const dk_view* views) {
   if (plans.size() < 2 || getenv("DK_JIT_SPLIT_NESTS")) return false;
+  static const int64_t cap = [] {
+    const char* e = getenv("DK_JIT_MERGE_MAX");
+    return e ? atoll(e) : (int64_t)1 << 21;
+  }();
   size_t bytes = 8 + 4 * (plans.size() + 1);
-  for (const NestPlan& np : plans) {
+  for (size_t n = 0; n < plans.size(); ++n) {
+    const NestPlan& np = plans[n];
+    const dk_view& dv = views[g.nests[n].dom];
+    int64_t ne = 1;
+    for (int d = 0; d < np.rank; ++d) ne *= dv.ext[d];
+    if (ne > cap) return false;
     if (np.rank > 0 && (!np.oneshot || np.staged || np.sweep)) return false;
     bytes += sizeof(DkHdr) + (np.red_slots.empty() ? 0 : sizeof(DkPub)) + 48 * std::max<size_t>(np.sites.size(), 1) +
              sizeof(dk_view) * std::max<size_t>(np.red_slots.size(), 1) + 8 * std::max(g.nscal, 1);
@@ -1754,13 +1766,15 @@ static Module* get_module(KernelObj& k, const dk_view* views, const double* scal
       }
     key += "s" + std::to_string(rep[i]);
   }
+  const bool merge = mergeable(k.prog, plans, views);
+  key += merge ? "M" : "S";
   auto it = k.mods.find(key);
   if (it != k.mods.end()) return it->second.get();
   auto m = std::make_unique<Module>();
   char name[32];
   snprintf(name, sizeof name, "dkf_%08llx", (unsigned long long)(fnv1a(k.text) & 0xffffffffull));
   GenOpts opts = default_opts(plans);
-  opts.merged = m->merged = mergeable(k.prog, plans);
+  opts.merged = m->merged = merge;
   std::vector<CUfunction> fns;
   for (;;) {
     Gen gen(k.prog, plans, name, opts, rep);
@@ -2077,7 +2091,7 @@ int dk_kernel_codegen(const char* program, int64_t len, const dk_view* views, in
         }
     }
     GenOpts opts = default_opts(plans);
-    opts.merged = mergeable(g, plans);
+    opts.merged = mergeable(g, plans, views);
     Gen gen(g, plans, "dk", opts, rep);
     std::string src = gen.source();
     if (compile) {
