@@ -228,7 +228,7 @@ def test_overlapped_halo_spmv_four_ranks():
     assert all(r[3] > 0 for r in res), res  # steady iterations replay the recorded overlap plan
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_spmv_dot_epilogue_across_ranks(world):
     """DK_FUSE_SPMV_DOT on several GPUs: each rank's SpMV (plain, or the overlapped-halo split into
     three row spans) emits p.q partials; the next window folds them into its own peer-board block
@@ -236,6 +236,8 @@ def test_spmv_dot_epilogue_across_ranks(world):
     reference within rtol 1e-12 (p.q is summed in another order)."""
     if world == 2:
         names = ["cg_csr_8x8_k2/fused", "pcg_csr_8x8_k2/fused", "cg_csr_6x12_k4/fused"]
+    elif world == 8:
+        names = [t for t in _k8_traces() if "_k8/fused" in t["meta"]["name"] and "cg" in t["meta"]["name"]]
     else:
         # + a 2-point plan on 4 ranks: two ranks own no point, so the epilogue must stay off
         names = [t for t in _k8_traces() if "_k4/fused" in t["meta"]["name"]] + ["cg_csr_8x8_k2/fused"]
@@ -243,7 +245,7 @@ def test_spmv_dot_epilogue_across_ranks(world):
     bad = [b for _, bs, *_ in res for b in bs]
     assert not bad, bad[:10]
     assert all(r[4] >= 3 for r in res), res
-    if world == 4:  # steady iterations (SpMV with the epilogue and its consumer) replayed from the plan cache
+    if world >= 4:  # steady iterations (SpMV with the epilogue and its consumer) replayed from the plan cache
         assert all(r[5] > 0 for r in res), res
 
 
