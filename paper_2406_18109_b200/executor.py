@@ -439,12 +439,24 @@ class Executor:
                 nbytes = sum(rg.volume(t[1]) * self.stores[t[0]].esize for t in mine)
                 self._rec["xfer"] = (n, sids, peers, dirs, los, his, nbytes)
 
+    def _contiguous(self, sid, lo, hi) -> bool:
+        """A rect of a row-major store is one contiguous span: after its first dimension with
+        more than one index, every dimension is full."""
+        shape = self.stores[sid].shape
+        ext = [hi[d] - lo[d] for d in range(len(shape))]
+        for d in range(len(shape)):
+            if ext[d] > 1:
+                return all(lo[e] == 0 and hi[e] == shape[e] for e in range(d + 1, len(shape)))
+        return True
+
     def _exchange(self, n, sids, peers, dirs, los, his) -> None:
-        """Move the transfer list: pairs whose rects fit a peer mailbox go through peer memory
-        (dk_p2p_exchange), the rest through grouped NCCL send/recv.  The split is per peer pair and
-        computed from the replicated plan, so both ends of a pair decide alike."""
+        """Move the transfer list: pairs whose rects fit a peer mailbox go through peer memory --
+        by copy engine (dk_dma_send / dk_dma_recv, DK_P2P_HALO=2) or by one pack/unpack kernel
+        (dk_p2p_exchange, DK_P2P_HALO=1) -- the rest through grouped NCCL send/recv.  The split is
+        per peer pair and computed from the replicated plan, so both ends of a pair decide alike."""
         use = {}
-        if self._p2p and os.environ.get("DK_P2P_HALO", "0") == "1":
+        mode = os.environ.get("DK_P2P_HALO", "0")
+        if self._p2p and mode in ("1", "2"):
             per = {}
             for i in range(n):
                 key = (peers[i], dirs[i])
@@ -457,6 +469,9 @@ class Executor:
             for q in {peers[i] for i in range(n)}:
                 fits = all(per.get((q, d), (0, 0))[0] <= runtime.P2P_MAIL_BYTES and per.get((q, d), (0, 0))[1] <= 8
                            for d in (0, 1))
+                if mode == "2":
+                    fits = fits and all(self._contiguous(sids[i], los[4 * i:4 * i + 4], his[4 * i:4 * i + 4])
+                                        for i in range(n) if peers[i] == q)
                 use[q] = fits
         p2p_idx = [i for i in range(n) if use.get(peers[i])]
         nccl_idx = [i for i in range(n) if not use.get(peers[i])]
@@ -468,7 +483,16 @@ class Executor:
                     (c_int64 * (4 * m))(*[los[4 * i + d] for i in idx for d in range(4)]),
                     (c_int64 * (4 * m))(*[his[4 * i + d] for i in idx for d in range(4)]))
 
-        if p2p_idx:
+        if p2p_idx and mode == "2":
+            # sends first: a send waits only for the ack of the message two before, never for
+            # this exchange, so every rank's sends are posted before any rank waits on a receive
+            for d, fn in ((0, self.lib.dk_dma_send), (1, self.lib.dk_dma_recv)):
+                idx = [i for i in p2p_idx if dirs[i] == d]
+                if idx:
+                    m, s_, p_, _d, lo_, hi_ = sub(idx)
+                    check(fn(m, s_, p_, lo_, hi_))
+            self.stats.p2p_halos += 1
+        elif p2p_idx:
             check(self.lib.dk_p2p_exchange(*(sub(p2p_idx) if nccl_idx else (n, sids, peers, dirs, los, his))))
             self.stats.p2p_halos += 1
         if nccl_idx:
@@ -807,6 +831,8 @@ class Executor:
             self._exchange(n, (c_int64 * n)(*[sids[c] for c in cs]), peers, dirs, los, his)
             self.stats.transfers += n
             self.stats.bytes_moved += nbytes
+            if kp is not None:
+                self.mark("halo_done")
         if kp is None and hit.get("overlap") is not None:
             ov = hit["overlap"]
             d = ov.get("dot")
@@ -957,6 +983,8 @@ class Executor:
             moves = self._satisfy(halo_need, defer=True)
         else:
             self._satisfy(need)
+            if kp is not None:
+                self.mark("halo_done")
 
         mine = [i for i in range(V) if prank[i] == self.rank]
         if overlap:

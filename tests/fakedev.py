@@ -229,6 +229,12 @@ class FakeLib:
         return 0
 
     def dk_sync(self):
+        # copy-engine sends land without the receiver's help on a GPU; the stand-in's isends
+        # complete when the peer receives them -- a device sync waits for them
+        for h in getattr(self, "_dma_pending", []):
+            h.wait()
+        self._dma_pending = []
+        self._dma_keep = []
         return 0
 
     def dk_get_stream(self, ref):
@@ -545,14 +551,18 @@ class FakeLib:
         self._dma_pending = getattr(self, "_dma_pending", [])
         for q in sorted({peers[i] for i in range(n)}):
             items = [i for i in range(n) if peers[i] == q]
-            data = [np.ascontiguousarray(self._store_array(sids[i])[los[4 * i]:his[4 * i]]).astype(np.float64)
-                    for i in items]
+            data = [np.ascontiguousarray(self._store_array(sids[i])[self._rect_index(sids[i], los, his, i)])
+                    .astype(np.float64).reshape(-1) for i in items]
             msg = np.concatenate([[float(self.xsend.get(q, 0))]] + data)
             t = torch.from_numpy(msg.copy())
             self._dma_pending.append(dist.isend(t, q, tag=91000))
             self._dma_keep = getattr(self, "_dma_keep", []) + [t]
             self.xsend[q] = self.xsend.get(q, 0) + 1
         return 0
+
+    def _rect_index(self, sid, los, his, i):
+        nd = self._store_array(sid).ndim
+        return tuple(slice(los[4 * i + d], his[4 * i + d]) for d in range(nd))
 
     def dk_dma_recv(self, n, sids, peers, los, his):
         import torch
@@ -561,7 +571,8 @@ class FakeLib:
         self.xrecv = getattr(self, "xrecv", {})
         for q in sorted({peers[i] for i in range(n)}):
             items = [i for i in range(n) if peers[i] == q]
-            sizes = [his[4 * i] - los[4 * i] for i in items]
+            sizes = [int(np.prod([his[4 * i + d] - los[4 * i + d] for d in range(self._store_array(sids[i]).ndim)]))
+                     for i in items]
             t = torch.empty(1 + sum(sizes), dtype=torch.float64)
             dist.recv(t, q, tag=91000)
             msg = t.numpy()
@@ -569,7 +580,9 @@ class FakeLib:
                 raise AssertionError(f"rank {self.rank}: message {int(msg[0])} from {q}, expected {self.xrecv.get(q, 0)}")
             off = 1
             for i, sz in zip(items, sizes):
-                self._store_array(sids[i])[los[4 * i]:his[4 * i]] = msg[off:off + sz]
+                dst = self._store_array(sids[i])
+                ix = self._rect_index(sids[i], los, his, i)
+                dst[ix] = msg[off:off + sz].reshape(dst[ix].shape)
                 off += sz
             self.xrecv[q] = self.xrecv.get(q, 0) + 1
         for h in getattr(self, "_dma_pending", []):

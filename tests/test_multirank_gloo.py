@@ -84,6 +84,7 @@ def _worker(rank, world, port, names, q, p2p=False, fuse=False):
             else:
                 replay(ex, trace.events)
             got = {s: ex.get(s) for s in trace.live}
+            ex.sync()  # the stand-in's copy-engine sends complete when the peer receives them
             moved += (ex.stats.p2p_folds + ex.stats.p2p_halos) if p2p else ex.stats.transfers
             hits += ex.stats.mplan_hits
             fused += ex.spmv_dot_stats["consumed"]
@@ -247,6 +248,23 @@ def test_spmv_dot_epilogue_across_ranks(world):
     assert all(r[4] >= 3 for r in res), res
     if world >= 4:  # steady iterations (SpMV with the epilogue and its consumer) replayed from the plan cache
         assert all(r[5] > 0 for r in res), res
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_copy_engine_halos(world, monkeypatch):
+    """DK_P2P_HALO=2: halos that fit a peer mailbox (stencil rows, CSR x halos, replicated reads)
+    move by copy engine (dk_dma_send / dk_dma_recv, stand-in: gloo isend/recv) instead of NCCL;
+    heaps byte-identical to the reference / oracle."""
+    monkeypatch.setenv("DK_P2P_HALO", "2")
+    if world == 2:
+        names = ["stencil/fused", "stencil_bands_n8_k2/fused", "stencil_bands_n6_k4/fused", "jacobi/fused",
+                 "cg_csr_6x12_k4/fused", "edge_ragged_2d/fused"]
+    else:
+        names = [t for t in _k8_traces() if "_k4/" in t["meta"]["name"]] + ["stencil_bands_n6_k4/fused"]
+    res = _run(names, world=world, p2p=True)
+    bad = [b for _, bs, *_ in res for b in bs]
+    assert not bad, bad[:10]
+    assert all(r[2] > 0 for r in res), res
 
 
 def test_isolated_streams_two_ranks():
