@@ -220,7 +220,8 @@ class Executor:
             p = c_uint64()
             check(self.lib.dk_scratch_alloc(8 * runtime.SPMV_DOT_DOUBLES * have, byref(p)))
             check(self.lib.dk_memset_zero(p.value, 8 * runtime.SPMV_DOT_DOUBLES * have))
-            self._sd_buf = ptr, have = p.value, have
+            ptr = p.value
+            self._sd_buf = (ptr, have)
         return ptr
 
     def free(self, sid: int) -> None:
