@@ -194,7 +194,8 @@ int dk_launch_pub(int64_t handle, const dk_view* views, int nviews, const double
 /* dk_launch_pub whose point block holds nred_total totals of which the kernel writes
  * its own at [red_offset, red_offset + its reductions): the rest of the block was filled
  * earlier on the stream (dk_p2p_block) -- how the opt-in SpMV + partial-dot epilogue
- * publishes the SpMV's p.q total with the following window's reductions. */
+ * publishes the SpMV's p.q total with the following window's reductions (the
+ * DOT(p, q -> pq) of trace.py:384-386, combined in point order as executor.py:193-195). */
 int dk_launch_pub_ex(int64_t handle, const dk_view* views, int nviews, const double* scalars, int nscalars,
                      int64_t epoch, int point, int red_offset, int nred_total);
 /* device address of this rank's block for `point` in the board slot of `epoch`
