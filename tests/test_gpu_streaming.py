@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 def test_streamed_blackscholes_window_matches_oracle():
     from oracle.interp import OracleHeap, execute_step
-    from paper_2406_18109_b200.executor import Executor, replay
+    from paper_2406_18109_b200.executor import Executor
     from paper_2406_18109_b200.plan import PlanTrace
     from paper_2406_18109_b200.streaming import HostStreamer, pinned
 

@@ -1,7 +1,6 @@
 """Pin the CPU oracle against the reference's own outputs (golden fixtures)."""
 
 import numpy as np
-import pytest
 
 from conftest import golden_arrays, same_bits
 from oracle.interp import OracleHeap, replay, spmv_csr_rows
