@@ -204,3 +204,39 @@ def test_multi_nest_windows_compile_as_one_kernel(rt):
     finally:
         del os.environ["DK_JIT_SPLIT_NESTS"]
     assert src.count("__global__") == len(e.kernel.nests)
+
+
+def test_multi_nest_merge_size_cap():
+    """Nests above DK_JIT_MERGE_MAX elements keep one launch per nest (the saved launch is worth
+    less than the one-wave grid-stride walk there): with a cap of 0 every non-empty multi-nest window splits."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import ctypes, sys
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+from conftest import load_golden
+import test_codegen as tc
+from paper_2406_18109_b200.plan import PlanTrace
+try:
+    ctypes.CDLL("libcuda.so.1", mode=ctypes.RTLD_GLOBAL)
+except OSError:
+    ctypes.CDLL("/usr/local/cuda/lib64/stubs/libcuda.so", mode=ctypes.RTLD_GLOBAL)
+from paper_2406_18109_b200 import runtime
+runtime.load()
+n = 0
+for case in load_golden("fuzz250.json.gz")[::10]:
+    tr = PlanTrace.from_json(case["trace"])
+    for e in tr.execs():
+        if e.kernel is not None and len(e.kernel.nests) > 1:
+            src = tc.codegen(runtime, e.kernel, tc.views_for(runtime, e.task, e.kernel, tr.shapes), compile_=False)
+            assert src.count("__global__") == len(e.kernel.nests), src[-500:]
+            n += 1
+print("split", n)
+""" % (os.path.join(repo, "tests"), repo)
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, DK_JIT_MERGE_MAX="0"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert int(r.stdout.split()[-1]) >= 5, r.stdout
